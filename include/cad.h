@@ -1,0 +1,343 @@
+/*
+ * cad.h -- C-ABI of the B200-native core-attention (CA) hot path.
+ *
+ * Drop-in boundary for DistCA's CA path. The reference (`cadsim`, C++20) has
+ * a value-type C++ API and no FFI; every entry point below replaces one
+ * reference function (cited as P/<file>:<line>, P = /root/reference/proj) or
+ * one modeled device operation that the reference only simulates
+ * (P/src/sim.cpp:22-30 for the CA kernel, P/src/sim.cpp:69-125 for the
+ * dispatch/return windows).
+ *
+ * Conventions
+ *  - POD structs only; no C++ or torch types cross this boundary.
+ *  - Every function returns int status: CAD_OK (0) or a negative code. The
+ *    reference's C++ exceptions map to codes: ConfigError -> CAD_ERR_CONFIG,
+ *    DomainError -> CAD_ERR_DOMAIN (P/include/cadsim/types.hpp:18-27). The
+ *    message of the last error on the calling thread is cad_last_error().
+ *  - Nothing throws across the ABI.
+ *  - Scheduler calls are re-entrant and thread-safe (the reference's types
+ *    are immutable values, P/include/cadsim/types.hpp:30-31). Device calls
+ *    take an explicit cudaStream_t (passed as void*) and caller-owned
+ *    device buffers; one comm context per GPU and per thread.
+ */
+#ifndef CAD_H_
+#define CAD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAD_OK 0
+#define CAD_ERR_CONFIG (-1)
+#define CAD_ERR_DOMAIN (-2)
+#define CAD_ERR_CUDA (-3)
+#define CAD_ERR_NCCL (-4)
+#define CAD_ERR_CAPACITY (-5) /* caller buffer too small; *n holds the need */
+
+/* Layout, P/include/cadsim/types.hpp:99 */
+#define CAD_LAYOUT_CONTIGUOUS 0
+#define CAD_LAYOUT_HEAD_TAIL 1
+
+/* DistKind, P/include/cadsim/workload.hpp:13-19 */
+#define CAD_DIST_PRETRAIN_UPSAMPLED 0
+#define CAD_DIST_PROLONG_LIKE 1
+#define CAD_DIST_UNIFORM 2
+#define CAD_DIST_FIXED 3
+#define CAD_DIST_CUSTOM_HISTOGRAM 4
+
+/* ---------------------------------------------------------------------- */
+/* Descriptors                                                             */
+/* ---------------------------------------------------------------------- */
+
+/* cadsim::Item, P/include/cadsim/types.hpp:112-124. A CA-task extent:
+ * queries [q_begin,q_end) of document `doc` with causal context
+ * [0,kv_extent), kv_extent == q_end. */
+typedef struct cad_item {
+  int64_t doc;
+  int64_t q_begin;
+  int64_t q_end;
+  int64_t kv_extent;
+  int64_t ht_mirror;
+  int32_t home_device;
+  uint8_t layout; /* CAD_LAYOUT_* */
+  uint8_t pad_[3];
+} cad_item;
+
+/* cadsim::CATask, P/include/cadsim/types.hpp:131-137 */
+typedef struct cad_task {
+  cad_item item;
+  int32_t source_device;
+  int32_t assigned_server;
+  int64_t comm_bytes;   /* Q/KV dispatch bytes, 0 when served at home */
+  int64_t output_bytes; /* O return bytes, 0 when served at home */
+} cad_task;
+
+/* cadsim::SchedulerConfig, P/include/cadsim/scheduler.hpp:12-21 */
+typedef struct cad_sched_cfg {
+  double epsilon;
+  double e_threshold;
+  int64_t tile_size;
+  double alpha_ca;
+  int64_t size_q;
+  int64_t size_kv;
+  uint8_t double_query_head_tail;
+  uint8_t pad_[7];
+  int64_t max_moves;
+} cad_sched_cfg;
+
+/* cadsim::ServerLoad, P/include/cadsim/scheduler.hpp:23-30 (items are
+ * returned separately by cad_plan_server). */
+typedef struct cad_server_load {
+  int32_t device;
+  int32_t pad_;
+  double assigned_flops;
+  int64_t assigned_core;
+  int64_t n_items;
+  int64_t sent_bytes;
+  int64_t received_bytes;
+} cad_server_load;
+
+/* Scalar fields of cadsim::SchedulePlan, P/include/cadsim/scheduler.hpp:32-45 */
+typedef struct cad_plan_stats {
+  double target;
+  double max_load;
+  double min_load;
+  double epsilon_used;
+  int64_t total_comm_bytes;
+  int64_t total_output_bytes;
+  int64_t migrations;
+  int64_t splits;
+  int64_t rejected_small;
+  int64_t n_tasks;
+  int64_t n_servers;
+  int32_t tolerance_met;
+  int32_t pad_;
+} cad_plan_stats;
+
+/* cadsim::MigrationProposal, P/include/cadsim/scheduler.hpp:60-67 */
+typedef struct cad_proposal {
+  double delta_f_max;
+  cad_item shard;
+  cad_item remainders[2];
+  int32_t n_remainders;
+  int32_t whole_item;
+  int64_t v_comm;
+  double priority;
+} cad_proposal;
+
+/* cadsim::CommQuery / ShardChoice, P/include/cadsim/comm.hpp:41-60 */
+typedef struct cad_comm_query {
+  double delta_f_max;
+  double f_item;
+  int64_t L_q;
+  int64_t L_kv;
+  int64_t size_q;
+  int64_t size_kv;
+  uint8_t layout;
+  uint8_t pad_[7];
+  int64_t ht_mirror;
+} cad_comm_query;
+
+typedef struct cad_shard_choice {
+  int64_t n_q;
+  int64_t n_kv;
+  int64_t bytes;
+  int64_t core;
+} cad_shard_choice;
+
+/* cadsim::LengthDistribution, P/include/cadsim/workload.hpp:28-43 */
+typedef struct cad_length_dist {
+  int32_t kind; /* CAD_DIST_* */
+  int32_t pad_;
+  int64_t max_doc_len;
+  int64_t min_len_threshold;
+  uint64_t seed;
+  double log_mu;
+  double log_sigma;
+  double upsample_drop_prob;
+  double long_mix_weight;
+  double long_log_mu;
+  double long_log_sigma;
+  int64_t fixed_len;
+  int64_t uniform_min;
+  const int64_t* hist_len; /* custom_histogram: lengths */
+  const double* hist_p;    /* custom_histogram: weights */
+  int64_t hist_n;
+} cad_length_dist;
+
+/* cadsim::ServedTask, P/include/cadsim/sim.hpp:30-35, by task index. */
+typedef struct cad_served_task {
+  int64_t task_index; /* index into cad_plan_tasks() */
+  int64_t in_bytes;
+  int64_t out_bytes;
+  int32_t half; /* 0 = ping, 1 = pong */
+  int32_t pad_;
+} cad_served_task;
+
+typedef struct cad_plan cad_plan; /* opaque SchedulePlan */
+
+/* ---------------------------------------------------------------------- */
+/* Host: workload, cost, scheduler                                         */
+/* ---------------------------------------------------------------------- */
+
+const char* cad_last_error(void);
+const char* cad_version(void);
+
+void cad_sched_cfg_default(cad_sched_cfg* cfg); /* scheduler.hpp:12-21 defaults */
+void cad_length_dist_default(cad_length_dist* d); /* workload.hpp:28-43 defaults */
+
+/* validate_item, P/src/types.cpp:58-74 */
+int cad_validate_item(const cad_item* item);
+/* ca_flops_core, P/src/cost.cpp:32-44 */
+int cad_ca_flops_core(const cad_item* item, int64_t* core);
+/* exact_causal_pairs, P/src/oracle.cpp:50-54 (closed form) */
+int64_t cad_causal_pairs(int64_t n_q, int64_t n_kv);
+/* item_bytes / shard_bytes, P/src/scheduler.cpp:53-60, P/src/comm.cpp:35-42 */
+int cad_item_bytes(const cad_item* item, const cad_sched_cfg* cfg, int64_t* bytes);
+
+/* sample_batch, P/src/workload.cpp:67-84. Two-call: lengths may be NULL with
+ * cap 0 to learn *n_docs. */
+int cad_sample_batch(const cad_length_dist* dist, int64_t total_tokens,
+                     int64_t* lengths, int64_t cap, int64_t* n_docs);
+/* place_sequential + chunk_items, P/src/workload.cpp:86-124 and
+ * P/src/types.cpp:117-132: the contiguous items of every device chunk, in
+ * chunk order. */
+int cad_place_sequential(const int64_t* lengths, int64_t n_docs,
+                         int64_t n_devices, int64_t tokens_per_device,
+                         cad_item* items, int64_t cap, int64_t* n_items);
+
+/* target_load, P/src/scheduler.cpp:13-19 */
+int cad_target_load(const cad_item* items, int64_t n, int64_t n_servers,
+                    double alpha_ca, double* target);
+/* classify_servers, P/src/scheduler.cpp:21-34. Output arrays hold n entries. */
+int cad_classify_servers(const double* loads, int64_t n, double target,
+                         int32_t* surplus_dev, double* surplus_gap,
+                         int64_t* n_surplus, int32_t* deficit_dev,
+                         double* deficit_gap, int64_t* n_deficit);
+/* one_tile_slack, P/src/scheduler.cpp:36-49 */
+int cad_one_tile_slack(const cad_item* items, int64_t n,
+                       const cad_sched_cfg* cfg, double* slack);
+/* v_min_comm, P/src/comm.cpp:98-178 */
+int cad_v_min_comm(const cad_comm_query* q, int64_t tile, cad_shard_choice* out);
+/* propose_migration, P/src/scheduler.cpp:109-194. *has_value = 0 plays
+ * std::nullopt. */
+int cad_propose_migration(const cad_server_load* source,
+                          const cad_server_load* dest, const cad_item* item,
+                          double target, const cad_sched_cfg* cfg,
+                          cad_proposal* out, int32_t* has_value);
+
+/* schedule, P/src/scheduler.cpp:196-357 (bit-exact) */
+int cad_schedule(const cad_item* items, int64_t n, int64_t n_servers,
+                 const cad_sched_cfg* cfg, cad_plan** plan);
+/* schedule_pp_tick, P/src/scheduler.cpp:359-373: items[i] belongs to stage
+ * stage_of[i]; n_stages stages. */
+int cad_schedule_pp_tick(const cad_item* items, const int32_t* stage_of,
+                         int64_t n, int64_t n_stages, int64_t n_servers,
+                         const cad_sched_cfg* cfg, cad_plan** plan);
+int cad_plan_get_stats(const cad_plan* plan, cad_plan_stats* stats);
+int cad_plan_tasks(const cad_plan* plan, const cad_task** tasks, int64_t* n);
+int cad_plan_server(const cad_plan* plan, int64_t server, cad_server_load* load,
+                    const cad_item** items);
+/* plan_to_stream, P/src/scheduler.cpp:375-385. *needed = strlen + 1. */
+int cad_plan_to_text(const cad_plan* plan, char* buf, size_t cap, size_t* needed);
+void cad_plan_free(cad_plan* plan);
+
+/* device_plans_from_schedule (served/sent + assign_halves),
+ * P/src/sim.cpp:34-46,129-157 */
+int cad_device_plan(const cad_plan* plan, int32_t device,
+                    cad_served_task* served, int64_t cap_served,
+                    int64_t* n_served, cad_served_task* sent, int64_t cap_sent,
+                    int64_t* n_sent);
+
+/* ---------------------------------------------------------------------- */
+/* Device: the CA kernels (replace task_layer_seconds, P/src/sim.cpp:22-30) */
+/* ---------------------------------------------------------------------- */
+
+/* One CA task as the server's kernel sees it: q rows [q_off, q_off+n_q) of
+ * the packed Q/O/dO buffers attend to kv rows [kv_off, kv_off+kv_len) of the
+ * packed K/V buffers with a bottom-right causal mask: query i sees keys
+ * 0 .. kv_len-n_q+i (P/src/oracle.cpp:50-54). Requires kv_len >= n_q >= 1. */
+typedef struct cad_ca_task {
+  int64_t q_off;
+  int64_t n_q;
+  int64_t kv_off;
+  int64_t kv_len;
+} cad_ca_task;
+
+/* Packed THD layouts: Q/O/dO [q_rows][h_q][head_dim] bf16, K/V/dK/dV
+ * [kv_rows][h_kv][head_dim] bf16, LSE [h_q][q_rows] fp32 (natural log),
+ * dQ accumulated in fp32 workspace then written bf16. head_dim must be 128.
+ * softmax_scale <= 0 selects 1/sqrt(head_dim). */
+typedef struct cad_ca_shape {
+  int32_t h_q;
+  int32_t h_kv;
+  int32_t head_dim;
+  float softmax_scale;
+  int64_t q_rows;
+  int64_t kv_rows;
+} cad_ca_shape;
+
+typedef struct cad_ca_plan cad_ca_plan; /* device work list for a task set */
+
+typedef struct cad_ca_plan_info {
+  int64_t n_fwd_units;
+  int64_t n_bwd_units;
+  int64_t causal_pairs;   /* sum over tasks of exact causal pairs */
+  double fwd_flops;       /* 4 * d * h_q * pairs */
+  double bwd_flops;       /* 10 * d * h_q * pairs */
+  size_t workspace_bytes; /* bytes cad_ca_bwd needs */
+} cad_ca_plan_info;
+
+int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks,
+                       const cad_ca_shape* shape, cad_ca_plan** plan);
+int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info);
+int cad_ca_plan_destroy(cad_ca_plan* plan);
+
+/* Forward: O = softmax(scale * Q K^T + causal mask) V, LSE per (head, row). */
+int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
+               const void* v, void* o, float* lse, void* stream);
+
+/* Backward: dQ, dK, dV from Q, K, V, O, dO, LSE. dK/dV are accumulated
+ * (+=) only if accumulate != 0, else overwritten; rows of tasks sharing a
+ * KV prefix sum their contributions. workspace >= workspace_bytes. */
+int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
+               const void* v, const void* o, const float* lse, const void* dout,
+               void* dq, void* dk, void* dv, void* workspace, size_t ws_bytes,
+               void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Device: dispatch / return (replace layer_windows, P/src/sim.cpp:69-125)  */
+/* ---------------------------------------------------------------------- */
+
+typedef struct cad_comm cad_comm; /* one NCCL communicator per GPU */
+
+#define CAD_UNIQUE_ID_BYTES 128
+int cad_comm_unique_id(uint8_t id[CAD_UNIQUE_ID_BYTES]);
+int cad_comm_init(const uint8_t id[CAD_UNIQUE_ID_BYTES], int32_t rank,
+                  int32_t world, cad_comm** comm);
+int cad_comm_destroy(cad_comm* comm);
+
+/* Row gather: dst[i] = src[idx[i]] for rows of row_bytes (16-byte multiple). */
+int cad_gather_rows(const void* src, const int64_t* idx_dev, int64_t n_rows,
+                    int64_t row_bytes, void* dst, void* stream);
+/* Row scatter(-add): dst[idx[i]] (+)= src[i]; add uses fp32 rows. */
+int cad_scatter_rows(const void* src, const int64_t* idx_dev, int64_t n_rows,
+                     int64_t row_bytes, void* dst, void* stream);
+int cad_scatter_add_f32(const float* src, const int64_t* idx_dev, int64_t n_rows,
+                        int64_t row_elems, float* dst, void* stream);
+
+/* All-to-allv over the communicator (grouped ncclSend/ncclRecv), byte
+ * counts and displacements per peer, on `stream`. */
+int cad_alltoallv(cad_comm* comm, const void* send, const int64_t* send_bytes,
+                  const int64_t* send_displ, void* recv,
+                  const int64_t* recv_bytes, const int64_t* recv_displ,
+                  void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* CAD_H_ */

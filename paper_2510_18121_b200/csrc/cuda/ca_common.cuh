@@ -1,0 +1,63 @@
+// Shared definitions of the CA kernels: device task/work-unit records, the
+// plan object behind cad_ca_plan, and TMA tensor-map construction.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../../include/cad.h"
+
+namespace cad_dev {
+
+constexpr int kTile = 128;    // q rows and kv rows per tile
+constexpr int kHeadDim = 128; // d
+constexpr uint32_t kTileBytes = kTile * kHeadDim * 2;  // one bf16 128x128 tile
+
+// One CA task on the device (row offsets into the packed THD buffers).
+struct DevTask {
+  int32_t q_off, n_q, kv_off, kv_len;
+};
+
+// Forward work unit: `nh` query heads starting at head0 (same KV head) on
+// q tile `tile` of task `task`; it walks kv tiles 0..n_kv-1.
+struct FwdUnit {
+  int32_t task, tile;
+  int16_t head0, nh;
+  int32_t n_kv;
+};
+
+// Backward work unit: kv tile `tile` of task `task` for query heads
+// [head0, head0+nh) of one KV head; it walks q tiles q_lo..n_qt-1.
+struct BwdUnit {
+  int32_t task, tile;
+  int16_t head0, nh;
+  int32_t q_lo, n_qt;
+};
+
+}  // namespace cad_dev
+
+struct cad_ca_plan {
+  cad_ca_shape shape{};
+  std::vector<cad_dev::DevTask> tasks;
+  std::vector<cad_dev::FwdUnit> fwd_units;
+  std::vector<cad_dev::BwdUnit> bwd_units;
+  cad_dev::DevTask* d_tasks = nullptr;
+  cad_dev::FwdUnit* d_fwd = nullptr;
+  cad_dev::BwdUnit* d_bwd = nullptr;
+  int64_t pairs = 0;
+  int device = 0;
+  int num_sms = 148;
+};
+
+namespace cad_dev {
+
+// 3-D tiled map over a packed [rows][heads][128] bf16 buffer: box of
+// 64 d-values x 128 rows x 1 head, 128-byte swizzle. A 128x128 tile is two
+// boxes (d 0-63 and 64-127), landing as two 16 KB K-major SW128 planes.
+void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
+
+}  // namespace cad_dev

@@ -1,0 +1,185 @@
+// cad_ca_plan: the device work list of one CA task set (one server, one
+// nano-batch half), built once on the host and reused by every layer's
+// forward and backward launch.
+//
+// Work decomposition. Forward: one unit per (task, 128-row q tile, KV head,
+// pair of query heads of that KV head's GQA group); it walks the causal kv
+// tiles 0..n_kv-1 (tiles entirely above the diagonal are never visited).
+// Backward: one unit per (task, 128-row kv tile, KV head, pair of query
+// heads); it walks q tiles from the first one that can see the kv tile.
+// Units are sorted by length, longest first, so the persistent CTAs'
+// strided walk ends with the short units (LPT).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <type_traits>
+#include <numeric>
+#include <string>
+
+#include "../host/cad_status.hpp"
+#include "ca_common.cuh"
+
+namespace cad_dev {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw cad::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw cad::CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+}  // namespace
+
+void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads) {
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(heads)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(heads) * kHeadDim * 2,
+                                 static_cast<cuuint64_t>(kHeadDim) * 2};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kTile), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cad::CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+static void build_units(cad_ca_plan& P) {
+  const int hq = P.shape.h_q, hkv = P.shape.h_kv, group = hq / hkv;
+  const int per_unit = (group % 2 == 0) ? 2 : 1;  // query heads sharing one KV tile stream
+  for (int32_t t = 0; t < static_cast<int32_t>(P.tasks.size()); ++t) {
+    const DevTask& tk = P.tasks[t];
+    const int shift = tk.kv_len - tk.n_q;
+    const int n_qt = (tk.n_q + kTile - 1) / kTile;
+    const int n_kt = (tk.kv_len + kTile - 1) / kTile;
+    for (int i = 0; i < n_qt; ++i) {
+      const int last_pos = shift + std::min(tk.n_q, (i + 1) * kTile) - 1;
+      const int n_kv = last_pos / kTile + 1;
+      for (int hk = 0; hk < hkv; ++hk)
+        for (int g = 0; g < group; g += per_unit) {
+          FwdUnit u;
+          u.task = t;
+          u.tile = i;
+          u.head0 = static_cast<int16_t>(hk * group + g);
+          u.nh = static_cast<int16_t>(per_unit);
+          u.n_kv = n_kv;
+          P.fwd_units.push_back(u);
+        }
+    }
+    for (int j = 0; j < n_kt; ++j) {
+      // First q row whose position reaches key j*128: shift + qi >= j*128.
+      const int q_first = std::max(0, j * kTile - shift);
+      if (q_first >= tk.n_q) continue;  // unreachable for kv_len >= n_q, kept for safety
+      for (int hk = 0; hk < hkv; ++hk)
+        for (int g = 0; g < group; g += per_unit) {
+          BwdUnit u;
+          u.task = t;
+          u.tile = j;
+          u.head0 = static_cast<int16_t>(hk * group + g);
+          u.nh = static_cast<int16_t>(per_unit);
+          u.q_lo = q_first / kTile;
+          u.n_qt = n_qt;
+          P.bwd_units.push_back(u);
+        }
+    }
+  }
+  std::stable_sort(P.fwd_units.begin(), P.fwd_units.end(),
+                   [](const FwdUnit& a, const FwdUnit& b) { return a.n_kv > b.n_kv; });
+  std::stable_sort(P.bwd_units.begin(), P.bwd_units.end(), [](const BwdUnit& a, const BwdUnit& b) {
+    return (a.n_qt - a.q_lo) > (b.n_qt - b.q_lo);
+  });
+}
+
+}  // namespace cad_dev
+
+using cad_dev::cuda_check;
+
+extern "C" {
+
+int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_shape* shape,
+                       cad_ca_plan** plan) {
+  return cad::guarded([&] {
+    if (!shape || !plan || (n_tasks > 0 && !tasks) || n_tasks < 0) throw cad::DomainError("null argument");
+    *plan = nullptr;
+    if (shape->head_dim != cad_dev::kHeadDim) throw cad::ConfigError("head_dim must be 128");
+    if (shape->h_q < 1 || shape->h_kv < 1 || shape->h_q % shape->h_kv != 0)
+      throw cad::ConfigError("h_q must be a positive multiple of h_kv");
+    if (shape->q_rows < 0 || shape->kv_rows < 0 || shape->q_rows >= (int64_t(1) << 31) ||
+        shape->kv_rows >= (int64_t(1) << 31))
+      throw cad::ConfigError("row counts out of range");
+    auto P = std::make_unique<cad_ca_plan>();
+    P->shape = *shape;
+    if (!(P->shape.softmax_scale > 0)) P->shape.softmax_scale = 1.0f / std::sqrt(float(shape->head_dim));
+    for (int64_t i = 0; i < n_tasks; ++i) {
+      const cad_ca_task& t = tasks[i];
+      if (t.n_q < 1 || t.kv_len < t.n_q) throw cad::DomainError("CA task needs kv_len >= n_q >= 1");
+      if (t.q_off < 0 || t.q_off + t.n_q > shape->q_rows || t.kv_off < 0 ||
+          t.kv_off + t.kv_len > shape->kv_rows)
+        throw cad::DomainError("CA task rows outside the buffers");
+      P->tasks.push_back({static_cast<int32_t>(t.q_off), static_cast<int32_t>(t.n_q),
+                          static_cast<int32_t>(t.kv_off), static_cast<int32_t>(t.kv_len)});
+      P->pairs += cad_causal_pairs(t.n_q, t.kv_len);
+    }
+    cad_dev::build_units(*P);
+    cuda_check(cudaGetDevice(&P->device), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device),
+               "cudaDeviceGetAttribute");
+    auto upload = [](auto& vec, auto** dst) {
+      using T = typename std::decay_t<decltype(vec)>::value_type;
+      const size_t bytes = std::max<size_t>(1, vec.size()) * sizeof(T);
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(dst), bytes), "cudaMalloc(plan)");
+      if (!vec.empty())
+        cuda_check(cudaMemcpy(*dst, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice),
+                   "cudaMemcpy(plan)");
+    };
+    upload(P->tasks, &P->d_tasks);
+    upload(P->fwd_units, &P->d_fwd);
+    upload(P->bwd_units, &P->d_bwd);
+    *plan = P.release();
+  });
+}
+
+int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info) {
+  return cad::guarded([&] {
+    if (!plan || !info) throw cad::DomainError("null argument");
+    info->n_fwd_units = static_cast<int64_t>(plan->fwd_units.size());
+    info->n_bwd_units = static_cast<int64_t>(plan->bwd_units.size());
+    info->causal_pairs = plan->pairs;
+    const double base = double(plan->shape.head_dim) * double(plan->shape.h_q) * double(plan->pairs);
+    info->fwd_flops = 4.0 * base;
+    info->bwd_flops = 10.0 * base;
+    // dQ fp32 accumulator + delta = rowsum(dO*O) per (head, row)
+    info->workspace_bytes = size_t(plan->shape.q_rows) * plan->shape.h_q * (plan->shape.head_dim + 1) * 4;
+  });
+}
+
+int cad_ca_plan_destroy(cad_ca_plan* plan) {
+  return cad::guarded([&] {
+    if (!plan) return;
+    cudaFree(plan->d_tasks);
+    cudaFree(plan->d_fwd);
+    cudaFree(plan->d_bwd);
+    delete plan;
+  });
+}
+
+}  // extern "C"
