@@ -1,0 +1,680 @@
+// CA backward on sm_100a: dQ, dK, dV of O = softmax(scale Q K^T + mask) V
+// over the server's CA-tasks, recomputing P from the forward's LSE (no
+// materialised P).
+//
+// Three launches, all deterministic (no atomics):
+//   1. ca_delta:   D[h][row] = sum_d dO * O (fp32).
+//   2. ca_bwd_dkdv: one unit per (KV group, kv tile, KV head). For every
+//      query head of the GQA group and every q tile that can see the kv tile:
+//        S^T = K Q^T, dP^T = V dO^T                        (tcgen05 -> TMEM)
+//        P^T = exp(S^T - LSE), dS^T = P^T (dP^T - D)      (2 warpgroups, bf16
+//                                                          written back to TMEM)
+//        dV += P^T dO, dK += dS^T Q                        (A operand in TMEM)
+//      dK/dV stay in TMEM for the whole unit and are stored once (bf16).
+//   3. ca_bwd_dq: one unit per (task, q tile, query head), walking its kv
+//      tiles: S = Q K^T, dP = dO V^T, dS = P (dP - D), dQ += dS K; dQ stays in
+//      TMEM and is stored once.
+// The dQ pass recomputes S and dP (7 tile GEMMs instead of 5) in exchange for
+// no fp32 dQ atomics and exact determinism.
+//
+// Both main kernels: 12 warps = softmax-like warpgroups 0 and 1 (columns
+// 0-63 and 64-127 of each 128x128 tile, thread = TMEM lane = tile row),
+// control warpgroup 2 (warp 8 TMA producer, warp 9 MMA issuer).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "../host/cad_status.hpp"
+#include "ca_common.cuh"
+#include "ca_mma.cuh"
+#include "sm100.cuh"
+
+namespace cad_dev {
+namespace bwd {
+
+constexpr int kThreads = 384;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void load_row64(uint32_t taddr, float (&x)[64]) {
+  uint32_t r[32];
+  tmem_ld32(taddr, r);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+  tmem_ld32(taddr + 32, r);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[32 + i] = __uint_as_float(r[i]);
+  tmem_wait_ld();
+}
+
+// 64 fp32 -> 32 packed bf16x2 columns at taddr.
+__device__ __forceinline__ void store_bf16_64(uint32_t taddr, const float (&x)[64]) {
+  uint32_t pk[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
+  tmem_st32(taddr, pk);
+}
+
+// Epilogue helper: TMEM row (64 fp32 columns at taddr) * mul -> bf16 -> 128
+// contiguous bytes at dst (if valid).
+__device__ __forceinline__ void tmem_row_to_global(uint32_t taddr, float mul, __nv_bfloat16* dst,
+                                                   bool valid) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    uint4 w[4];
+    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * mul, __uint_as_float(r[2 * i + 1]) * mul);
+    if (valid) {
+      uint4* d = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = w[i];
+    }
+  }
+}
+
+// ============================================================== D = rowsum
+// One warp per (row, head): 128 bf16 of dO and O, lanes take 4 each. Also
+// re-lays the forward's LSE as log2-domain rows with a 16-byte-aligned pitch
+// so the dK/dV kernel can TMA both per q tile.
+__global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bfloat16* o,
+                                const __nv_bfloat16* dout, const float* lse, float* delta,
+                                float* lse2, int h_q, int64_t q_rows, int64_t pitch) {
+  const int warps_per_block = blockDim.x / 32;
+  const int64_t gw = int64_t(blockIdx.x) * warps_per_block + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  // rows are enumerated task by task
+  int64_t rem = gw / h_q;
+  const int h = static_cast<int>(gw % h_q);
+  for (int t = 0; t < n_tasks; ++t) {
+    if (rem < tasks[t].n_q) {
+      const int64_t row = tasks[t].q_off + rem;
+      const int64_t base = (row * h_q + h) * kHeadDim + lane * 4;
+      const uint2 a = *reinterpret_cast<const uint2*>(o + base);
+      const uint2 b = *reinterpret_cast<const uint2*>(dout + base);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 fa = __bfloat1622float2(a2[i]);
+        const float2 fb = __bfloat1622float2(b2[i]);
+        s += fa.x * fb.x + fa.y * fb.y;
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) {
+        delta[int64_t(h) * pitch + row] = s;
+        lse2[int64_t(h) * pitch + row] = lse[int64_t(h) * q_rows + row] * kLog2e;
+      }
+      return;
+    }
+    rem -= tasks[t].n_q;
+  }
+}
+
+// ============================================================== dK / dV
+namespace kv {
+
+constexpr uint32_t kKOff = 0;
+constexpr uint32_t kVOff = kTileBytes;
+constexpr uint32_t kQOff = 2 * kTileBytes;   // 2 stages
+constexpr uint32_t kDOOff = 4 * kTileBytes;  // 2 stages
+constexpr uint32_t kRowOff = 6 * kTileBytes; // [stage][LSE 128 | D 128] fp32
+constexpr uint32_t kBarOff = kRowOff + 4 * 512;
+constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+
+struct Bars {
+  uint64_t kv_full, kv_empty;
+  uint64_t in_full[2], in_empty[2];
+  uint64_t s_full, dp_full, p_full, ds_full, acc_full, acc_free;
+  uint32_t tmem_base;
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;
+  const float* lse2;   // log2-domain LSE, [h_q][pitch]
+  const float* delta;  // [h_q][pitch]
+  int64_t pitch;
+  const DevTask* tasks;
+  const KvUnit* units;
+  const KvSeg* segs;
+  int n_units;
+  int group;
+  int h_kv;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  float scale;       // softmax scale (dK multiplier)
+  float scale_log2;  // softmax scale * log2(e)
+};
+
+// Iteration cursor over (head in group, segment, q tile) of one unit.
+struct Cursor {
+  int g, seg, qt;
+  __device__ void start(const KvUnit& u, const KvSeg* segs) {
+    g = 0;
+    seg = u.seg_begin;
+    qt = segs[seg].qt_lo;
+  }
+  __device__ void next(const KvUnit& u, const KvSeg* segs) {
+    if (++qt < segs[seg].qt_hi) return;
+    if (++seg < u.seg_end) {
+      qt = segs[seg].qt_lo;
+      return;
+    }
+    ++g;
+    seg = u.seg_begin;
+    qt = segs[seg].qt_lo;
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+  float* rows = reinterpret_cast<float*>(smem + kRowOff);  // [stage][lse 128 | d 128]
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&p.tm_q);
+    tma_prefetch(&p.tm_k);
+    tma_prefetch(&p.tm_v);
+    tma_prefetch(&p.tm_do);
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->in_full[i], 33);
+      mbar_init(&bars->in_empty[i], 1);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_full, 256);
+    mbar_init(&bars->ds_full, 256);
+    mbar_init(&bars->acc_full, 1);
+    mbar_init(&bars->acc_free, 256);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  // TMEM: S^T [0,128)  dP^T [128,256)  dV [256,384)  dK [384,512)
+  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (warp == 8) {
+      // ---------------------------------------------------------- producer
+      // Lane 0 issues the TMA tile loads; the whole warp copies the tile's
+      // 128 LSE and 128 D values (arbitrary, unaligned row offsets) into
+      // shared memory with plain loads and arrives on in_full (count 33).
+      uint32_t kv_it = 0, st = 0, ph = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const KvUnit un = p.units[u];
+        const int krow = un.kv_off + un.tile * kTile;
+        if (lane == 0) {
+          mbar_wait(&bars->kv_empty, (kv_it & 1) ^ 1);
+          mbar_expect_tx(&bars->kv_full, 2 * kTileBytes);
+          tma_load_3d(&p.tm_k, &bars->kv_full, smem + kKOff, 0, krow, un.hk);
+          tma_load_3d(&p.tm_k, &bars->kv_full, smem + kKOff + kTileBytes / 2, 64, krow, un.hk);
+          tma_load_3d(&p.tm_v, &bars->kv_full, smem + kVOff, 0, krow, un.hk);
+          tma_load_3d(&p.tm_v, &bars->kv_full, smem + kVOff + kTileBytes / 2, 64, krow, un.hk);
+        }
+        ++kv_it;
+        Cursor c;
+        c.start(un, p.segs);
+        for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
+          const DevTask tk = p.tasks[p.segs[c.seg].task];
+          const int head = un.hk * p.group + c.g;
+          const int qrow = tk.q_off + c.qt * kTile;
+          mbar_wait(&bars->in_empty[st], ph ^ 1);
+          if (lane == 0) {
+            mbar_expect_tx(&bars->in_full[st], 2 * kTileBytes);
+            uint8_t* q = smem + kQOff + st * kTileBytes;
+            uint8_t* d = smem + kDOOff + st * kTileBytes;
+            tma_load_3d(&p.tm_q, &bars->in_full[st], q, 0, qrow, head);
+            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kTileBytes / 2, 64, qrow, head);
+            tma_load_3d(&p.tm_do, &bars->in_full[st], d, 0, qrow, head);
+            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kTileBytes / 2, 64, qrow, head);
+          }
+          float* dst = rows + st * 256;
+          const int64_t hbase = int64_t(head) * p.pitch;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int col = lane + 32 * k;
+            const int64_t rrow = int64_t(qrow) + col;
+            const bool in = rrow < p.pitch;
+            dst[col] = in ? p.lse2[hbase + rrow] : 0.f;
+            dst[128 + col] = in ? p.delta[hbase + rrow] : 0.f;
+          }
+          mbar_arrive(&bars->in_full[st]);
+          if (++st == 2) { st = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 9 && lane == 0) {
+      // ---------------------------------------------------------- MMA
+      uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0;
+      uint32_t p_ph = 0, ds_ph = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const KvUnit un = p.units[u];
+        const int n = un.n_iter;
+        mbar_wait(&bars->kv_full, kv_it & 1);
+        ++kv_it;
+        mbar_wait(&bars->in_full[st], ph);
+        tc_fence_after();
+        const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
+        uint32_t sQ = sbase + kQOff + st * kTileBytes, sDO = sbase + kDOOff + st * kTileBytes;
+        issue_qk(tS, sK, sQ);
+        umma_commit(&bars->s_full);
+        issue_qk(tDP, sV, sDO);
+        umma_commit(&bars->dp_full);
+        for (int i = 0; i < n; ++i) {
+          const uint32_t cur_st = st;
+          mbar_wait(&bars->p_full, p_ph);
+          p_ph ^= 1;
+          if (i == 0) {
+            mbar_wait(&bars->acc_free, (acc_it & 1) ^ 1);
+            ++acc_it;
+          }
+          tc_fence_after();
+          issue_pv(tDV, tS, tS + 64, sDO, i > 0);  // dV += P^T dO
+          uint32_t nQ = 0, nDO = 0;
+          if (i + 1 < n) {
+            if (++st == 2) { st = 0; ph ^= 1; }
+            mbar_wait(&bars->in_full[st], ph);
+            tc_fence_after();
+            nQ = sbase + kQOff + st * kTileBytes;
+            nDO = sbase + kDOOff + st * kTileBytes;
+            issue_qk(tS, sK, nQ);  // S^T(i+1)
+            umma_commit(&bars->s_full);
+          }
+          mbar_wait(&bars->ds_full, ds_ph);
+          ds_ph ^= 1;
+          tc_fence_after();
+          issue_pv(tDK, tDP, tDP + 64, sQ, i > 0);  // dK += dS^T Q
+          umma_commit(&bars->in_empty[cur_st]);
+          if (i + 1 < n) {
+            issue_qk(tDP, sV, nDO);  // dP^T(i+1)
+            umma_commit(&bars->dp_full);
+            sQ = nQ;
+            sDO = nDO;
+          }
+        }
+        umma_commit(&bars->acc_full);
+        umma_commit(&bars->kv_empty);
+        if (++st == 2) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ------------------------------------------------------------ elementwise
+    const int w = warp >> 2;                    // column half: q cols [64w, 64w+64)
+    const uint32_t r = (warp & 3) * 32 + lane;  // kv row within the tile
+    const uint32_t lsel = ((warp & 3) * 32) << 16;
+    const int c0 = 64 * w;
+    uint32_t st = 0, ph = 0, s_ph = 0, dp_ph = 0, acc_ph = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const KvUnit un = p.units[u];
+      const int kj = un.tile * kTile + r;  // key index relative to kv_off
+      Cursor c;
+      c.start(un, p.segs);
+      for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
+        const DevTask tk = p.tasks[p.segs[c.seg].task];
+        const int shift = tk.kv_len - tk.n_q;
+        const int q0 = c.qt * kTile + c0;  // query index of this thread's column 0
+        mbar_wait_warp(&bars->in_full[st], ph);
+        const float* lse = rows + st * 256 + c0;
+        const float* dd = rows + st * 256 + 128 + c0;
+        if (++st == 2) { st = 0; ph ^= 1; }
+        mbar_wait_warp(&bars->s_full, s_ph);
+        s_ph ^= 1;
+        tc_fence_after();
+        float x[64];
+        load_row64(tS + lsel + c0, x);
+        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q
+        const int lo = kj - shift - q0;        // first visible column
+        const int hi = tk.n_q - q0;            // columns >= hi are padding
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const float e = ex2(fmaf(x[k], p.scale_log2, -lse[k]));
+          x[k] = (k >= lo && k < hi) ? e : 0.f;
+        }
+        store_bf16_64(tS + lsel + 32 * w * 2, x);  // P^T: WG0 -> cols [0,32), WG1 -> [64,96)
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full);
+        mbar_wait_warp(&bars->dp_full, dp_ph);
+        dp_ph ^= 1;
+        tc_fence_after();
+        float y[64];
+        load_row64(tDP + lsel + c0, y);
+#pragma unroll
+        for (int k = 0; k < 64; ++k) y[k] = (k >= lo && k < hi) ? x[k] * (y[k] - dd[k]) : 0.f;
+        store_bf16_64(tDP + lsel + 32 * w * 2, y);  // dS^T
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->ds_full);
+      }
+      // ---- epilogue: this warpgroup stores d columns [c0, c0+64) of dV and dK
+      mbar_wait_warp(&bars->acc_full, acc_ph);
+      acc_ph ^= 1;
+      tc_fence_after();
+      const int row = un.kv_off + kj;
+      const bool valid = row < un.kv_end;
+      const int64_t off = (int64_t(row) * p.h_kv + un.hk) * kHeadDim + c0;
+      tmem_row_to_global(tDV + lsel + c0, 1.f, p.dv + off, valid);
+      tmem_row_to_global(tDK + lsel + c0, p.scale, p.dk + off, valid);
+      tc_fence_before();
+      mbar_arrive(&bars->acc_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_free<512>(tmem);
+}
+
+}  // namespace kv
+
+// ============================================================== dQ
+namespace dq {
+
+constexpr uint32_t kQOff = 0;
+constexpr uint32_t kDOOff = kTileBytes;
+constexpr uint32_t kKOff = 2 * kTileBytes;  // 2 stages
+constexpr uint32_t kVOff = 4 * kTileBytes;  // 2 stages
+constexpr uint32_t kBarOff = 6 * kTileBytes;
+constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+
+struct Bars {
+  uint64_t q_full, q_empty;
+  uint64_t kv_full[2], kv_empty[2];
+  uint64_t s_full, dp_full, p_read, ds_full, dq_full, dq_free;
+  uint32_t tmem_base;
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;
+  const DevTask* tasks;
+  const FwdUnit* units;
+  int n_units;
+  int group;
+  int h_q;
+  const float* lse2;   // log2-domain LSE, [h_q][pitch]
+  const float* delta;  // [h_q][pitch]
+  __nv_bfloat16* dq;
+  int64_t pitch;
+  float scale;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&p.tm_q);
+    tma_prefetch(&p.tm_k);
+    tma_prefetch(&p.tm_v);
+    tma_prefetch(&p.tm_do);
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_read, 256);
+    mbar_init(&bars->ds_full, 256);
+    mbar_init(&bars->dq_full, 1);
+    mbar_init(&bars->dq_free, 256);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  // TMEM: S [0,128)  dP [128,256)  dQ [256,384)  dS buffers [384,448) [448,512)
+  const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 384;
+
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (warp == 8 && lane == 0) {
+      uint32_t q_it = 0, st = 0, ph = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const FwdUnit un = p.units[u];
+        const DevTask tk = p.tasks[un.task];
+        const int hk = un.head0 / p.group;
+        const int qrow = tk.q_off + un.tile * kTile;
+        mbar_wait(&bars->q_empty, (q_it & 1) ^ 1);
+        ++q_it;
+        mbar_expect_tx(&bars->q_full, 2 * kTileBytes);
+        tma_load_3d(&p.tm_q, &bars->q_full, smem + kQOff, 0, qrow, un.head0);
+        tma_load_3d(&p.tm_q, &bars->q_full, smem + kQOff + kTileBytes / 2, 64, qrow, un.head0);
+        tma_load_3d(&p.tm_do, &bars->q_full, smem + kDOOff, 0, qrow, un.head0);
+        tma_load_3d(&p.tm_do, &bars->q_full, smem + kDOOff + kTileBytes / 2, 64, qrow, un.head0);
+        for (int j = 0; j < un.n_kv; ++j) {
+          const int krow = tk.kv_off + j * kTile;
+          mbar_wait(&bars->kv_empty[st], ph ^ 1);
+          mbar_expect_tx(&bars->kv_full[st], 2 * kTileBytes);
+          uint8_t* k = smem + kKOff + st * kTileBytes;
+          uint8_t* v = smem + kVOff + st * kTileBytes;
+          tma_load_3d(&p.tm_k, &bars->kv_full[st], k, 0, krow, hk);
+          tma_load_3d(&p.tm_k, &bars->kv_full[st], k + kTileBytes / 2, 64, krow, hk);
+          tma_load_3d(&p.tm_v, &bars->kv_full[st], v, 0, krow, hk);
+          tma_load_3d(&p.tm_v, &bars->kv_full[st], v + kTileBytes / 2, 64, krow, hk);
+          if (++st == 2) { st = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 9 && lane == 0) {
+      uint32_t q_it = 0, st = 0, ph = 0, dq_it = 0, pr_ph = 0, ds_ph = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const FwdUnit un = p.units[u];
+        const int n = un.n_kv;
+        mbar_wait(&bars->q_full, q_it & 1);
+        ++q_it;
+        mbar_wait(&bars->kv_full[st], ph);
+        tc_fence_after();
+        const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
+        issue_qk(tS, sQ, sbase + kKOff + st * kTileBytes);
+        umma_commit(&bars->s_full);
+        issue_qk(tDP, sDO, sbase + kVOff + st * kTileBytes);
+        umma_commit(&bars->dp_full);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t cur = st;
+          uint32_t nst = st, nph = ph;
+          if (j + 1 < n) {
+            if (++nst == 2) { nst = 0; nph ^= 1; }
+            mbar_wait(&bars->p_read, pr_ph);
+            pr_ph ^= 1;
+            mbar_wait(&bars->kv_full[nst], nph);
+            tc_fence_after();
+            issue_qk(tS, sQ, sbase + kKOff + nst * kTileBytes);  // S(j+1)
+            umma_commit(&bars->s_full);
+          } else {
+            mbar_wait(&bars->p_read, pr_ph);
+            pr_ph ^= 1;
+          }
+          mbar_wait(&bars->ds_full, ds_ph);
+          ds_ph ^= 1;
+          if (j == 0) {
+            mbar_wait(&bars->dq_free, (dq_it & 1) ^ 1);
+            ++dq_it;
+          }
+          tc_fence_after();
+          const uint32_t ds = tDS + (j & 1) * 64;
+          issue_pv(tDQ, ds, ds + 32, sbase + kKOff + cur * kTileBytes, j > 0);  // dQ += dS K
+          umma_commit(&bars->kv_empty[cur]);
+          if (j + 1 < n) {
+            issue_qk(tDP, sDO, sbase + kVOff + nst * kTileBytes);  // dP(j+1)
+            umma_commit(&bars->dp_full);
+          }
+          st = nst;
+          ph = nph;
+        }
+        umma_commit(&bars->dq_full);
+        umma_commit(&bars->q_empty);
+        if (++st == 2) { st = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    const int w = warp >> 2;                    // kv column half [64w, 64w+64)
+    const uint32_t r = (warp & 3) * 32 + lane;  // q row within the tile
+    const uint32_t lsel = ((warp & 3) * 32) << 16;
+    const int c0 = 64 * w;
+    uint32_t s_ph = 0, dp_ph = 0, dq_ph = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const FwdUnit un = p.units[u];
+      const DevTask tk = p.tasks[un.task];
+      const int shift = tk.kv_len - tk.n_q;
+      const int qi = un.tile * kTile + r;
+      const bool valid = qi < tk.n_q;
+      const int64_t row = int64_t(tk.q_off) + qi;
+      const float lse2 = valid ? p.lse2[int64_t(un.head0) * p.pitch + row] : 0.f;
+      const float dd = valid ? p.delta[int64_t(un.head0) * p.pitch + row] : 0.f;
+      const int pos = valid ? shift + qi : -1;  // invalid rows see nothing
+      for (int j = 0; j < un.n_kv; ++j) {
+        mbar_wait_warp(&bars->s_full, s_ph);
+        s_ph ^= 1;
+        tc_fence_after();
+        float x[64];
+        load_row64(tS + lsel + c0, x);
+        tc_fence_before();
+        mbar_arrive(&bars->p_read);
+        const int lim = pos - (j * kTile + c0);  // last visible column
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const float e = ex2(fmaf(x[k], p.scale_log2, -lse2));
+          x[k] = k <= lim ? e : 0.f;
+        }
+        mbar_wait_warp(&bars->dp_full, dp_ph);
+        dp_ph ^= 1;
+        tc_fence_after();
+        float y[64];
+        load_row64(tDP + lsel + c0, y);
+#pragma unroll
+        for (int k = 0; k < 64; ++k) y[k] = x[k] * (y[k] - dd);
+        store_bf16_64(tDS + lsel + (j & 1) * 64 + 32 * w, y);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars->ds_full);
+      }
+      mbar_wait_warp(&bars->dq_full, dq_ph);
+      dq_ph ^= 1;
+      tc_fence_after();
+      tmem_row_to_global(tDQ + lsel + c0, p.scale,
+                         p.dq + (row * p.h_q + un.head0) * kHeadDim + c0, valid);
+      tc_fence_before();
+      mbar_arrive(&bars->dq_free);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_free<512>(tmem);
+}
+
+}  // namespace dq
+}  // namespace bwd
+}  // namespace cad_dev
+
+extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k, const void* v,
+                          const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                          void* dv, void* workspace, size_t ws_bytes, void* stream) {
+  using namespace cad_dev;
+  using namespace cad_dev::bwd;
+  return cad::guarded([&] {
+    if (!plan || !q || !k || !v || !o || !lse || !dout || !dq || !dk || !dv || !workspace)
+      throw cad::DomainError("null argument");
+    const cad_ca_shape& sh = plan->shape;
+    const int64_t pitch = (sh.q_rows + 3) / 4 * 4;
+    const size_t need = size_t(2) * pitch * sh.h_q * 4;
+    if (ws_bytes < need) throw cad::DomainError("backward workspace too small");
+    if (plan->tasks.empty()) return;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static const bool debug_sync = std::getenv("CAD_DEBUG_SYNC") != nullptr;
+    float* delta = static_cast<float*>(workspace);
+    float* lse2 = delta + pitch * sh.h_q;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cuda_check(cudaFuncSetAttribute(kv::ca_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kv::kSmemBytes),
+                 "cudaFuncSetAttribute(dkdv)");
+      cuda_check(cudaFuncSetAttribute(dq::ca_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      dq::kSmemBytes),
+                 "cudaFuncSetAttribute(dq)");
+      attr_set = true;
+    }
+    // 1. D = rowsum(dO * O)
+    int64_t rows = 0;
+    for (const DevTask& t : plan->tasks) rows += t.n_q;
+    const int64_t warps = rows * sh.h_q;
+    const int per_block = 8;
+    ca_delta_kernel<<<static_cast<unsigned>((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
+        plan->d_tasks, static_cast<int>(plan->tasks.size()), static_cast<const __nv_bfloat16*>(o),
+        static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, sh.h_q, sh.q_rows, pitch);
+    cuda_check(cudaGetLastError(), "ca_delta launch");
+    if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
+    // 2. dK, dV
+    if (!plan->kv_units.empty()) {
+      kv::Params p;
+      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
+      make_tile_map(&p.tm_v, v, sh.kv_rows, sh.h_kv);
+      p.lse2 = lse2;
+      p.delta = delta;
+      p.pitch = pitch;
+      p.tasks = plan->d_tasks;
+      p.units = plan->d_kv;
+      p.segs = plan->d_segs;
+      p.n_units = static_cast<int>(plan->kv_units.size());
+      p.group = sh.h_q / sh.h_kv;
+      p.h_kv = sh.h_kv;
+      p.dk = static_cast<__nv_bfloat16*>(dk);
+      p.dv = static_cast<__nv_bfloat16*>(dv);
+      p.scale = sh.softmax_scale;
+      p.scale_log2 = sh.softmax_scale * kLog2e;
+      const int grid = std::min<int>(p.n_units, plan->num_sms);
+      kv::ca_bwd_dkdv_kernel<<<grid, kThreads, kv::kSmemBytes, s>>>(p);
+      cuda_check(cudaGetLastError(), "ca_bwd_dkdv launch");
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv");
+    }
+    // 3. dQ
+    {
+      dq::Params p;
+      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
+      make_tile_map(&p.tm_v, v, sh.kv_rows, sh.h_kv);
+      p.tasks = plan->d_tasks;
+      p.units = plan->d_dq;
+      p.n_units = static_cast<int>(plan->dq_units.size());
+      p.group = sh.h_q / sh.h_kv;
+      p.h_q = sh.h_q;
+      p.lse2 = lse2;
+      p.delta = delta;
+      p.dq = static_cast<__nv_bfloat16*>(dq);
+      p.pitch = pitch;
+      p.scale = sh.softmax_scale;
+      p.scale_log2 = sh.softmax_scale * kLog2e;
+      const int grid = std::min<int>(p.n_units, plan->num_sms);
+      dq::ca_bwd_dq_kernel<<<grid, kThreads, dq::kSmemBytes, s>>>(p);
+      cuda_check(cudaGetLastError(), "ca_bwd_dq launch");
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq");
+    }
+  });
+}

@@ -30,12 +30,20 @@ struct FwdUnit {
   int32_t n_kv;
 };
 
-// Backward work unit: kv tile `tile` of task `task` for query heads
-// [head0, head0+nh) of one KV head; it walks q tiles q_lo..n_qt-1.
-struct BwdUnit {
-  int32_t task, tile;
-  int16_t head0, nh;
-  int32_t q_lo, n_qt;
+// dK/dV work unit: kv tile `tile` of a KV group (the tasks sharing one KV
+// row range [kv_off, kv_end), e.g. the shards of one document on this
+// server) for KV head hk. It walks, for every query head of hk's GQA group,
+// the segments seg_begin..seg_end-1: (task, q tiles qt_lo..qt_hi-1) that
+// can see the tile. One unit owns its dK/dV rows, so no reduction across
+// units is needed.
+struct KvUnit {
+  int32_t kv_off, kv_end, tile;
+  int16_t hk, pad;
+  int32_t seg_begin, seg_end;
+  int32_t n_iter;  // group * sum of segment lengths
+};
+struct KvSeg {
+  int32_t task, qt_lo, qt_hi;
 };
 
 }  // namespace cad_dev
@@ -44,10 +52,14 @@ struct cad_ca_plan {
   cad_ca_shape shape{};
   std::vector<cad_dev::DevTask> tasks;
   std::vector<cad_dev::FwdUnit> fwd_units;
-  std::vector<cad_dev::BwdUnit> bwd_units;
+  std::vector<cad_dev::FwdUnit> dq_units;  // nh == 1
+  std::vector<cad_dev::KvUnit> kv_units;
+  std::vector<cad_dev::KvSeg> kv_segs;
   cad_dev::DevTask* d_tasks = nullptr;
   cad_dev::FwdUnit* d_fwd = nullptr;
-  cad_dev::BwdUnit* d_bwd = nullptr;
+  cad_dev::FwdUnit* d_dq = nullptr;
+  cad_dev::KvUnit* d_kv = nullptr;
+  cad_dev::KvSeg* d_segs = nullptr;
   int64_t pairs = 0;
   int device = 0;
   int num_sms = 148;
@@ -59,5 +71,8 @@ namespace cad_dev {
 // 64 d-values x 128 rows x 1 head, 128-byte swizzle. A 128x128 tile is two
 // boxes (d 0-63 and 64-127), landing as two 16 KB K-major SW128 planes.
 void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
+// 2-D map over a [heads][rows] fp32 buffer (LSE, D): box of 128 rows x 1 head.
+void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
+void cuda_check(cudaError_t e, const char* what);
 
 }  // namespace cad_dev

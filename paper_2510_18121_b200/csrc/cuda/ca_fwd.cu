@@ -33,6 +33,7 @@
 
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
+#include "ca_mma.cuh"
 #include "sm100.cuh"
 
 namespace cad_dev {
@@ -65,30 +66,6 @@ struct Params {
   int64_t q_rows;
   float scale_log2;  // softmax scale * log2(e)
 };
-
-// S = Q K^T: M=128 (q rows), N=128 (kv rows), K=128 (d) as 8 steps of 16.
-__device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint32_t q_smem, uint32_t k_smem) {
-  constexpr uint32_t idesc = idesc_bf16(128, 128, false, false);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t off = (k >> 2) * (kTileBytes / 2) + (k & 3) * 32;
-    umma_ss(d_tmem, sw128_desc(q_smem + off, 16, 1024), sw128_desc(k_smem + off, 16, 1024), idesc,
-            k > 0 ? 1u : 0u);
-  }
-}
-
-// O += P V: M=128 (q rows), N=128 (d), K=128 (kv rows) as 8 steps of 16.
-// P (bf16) sits in TMEM, 2 values per column; V is MN-major (d contiguous):
-// LBO = 16 KB between the two 64-wide d planes, SBO = 1 KB per 8 kv rows.
-__device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, uint32_t v_smem,
-                                         bool accumulate) {
-  constexpr uint32_t idesc = idesc_bf16(128, 128, false, true);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    umma_ts(d_tmem, p_tmem + k * 8, sw128_desc(v_smem + k * 2048, kTileBytes / 2, 1024), idesc,
-            (accumulate || k > 0) ? 1u : 0u);
-  }
-}
 
 __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -198,7 +175,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
               fph[h] ^= 1;
             }
             tc_fence_after();
-            issue_pv(tmem + 256 + h * 128, tmem + h * 128, sbase + kVOff + vs * kTileBytes, j > 0);
+            issue_pv(tmem + 256 + h * 128, tmem + h * 128, tmem + h * 128 + 32,
+                     sbase + kVOff + vs * kTileBytes, j > 0);
             if (j == n - 1) {
               umma_commit(&bars->o_full[h]);
             } else {
@@ -242,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < un.n_kv; ++j) {
         if (row == 0) dbg_mark(2 + h, 0x100 + j);
-        mbar_wait(&bars->s_full[h], sph);
+        mbar_wait_warp(&bars->s_full[h], sph);
         sph ^= 1;
         tc_fence_after();
         float s[128];
@@ -302,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
         if (row == 0) dbg_mark(2 + h, 0x200 + j);
       }
       // ---- epilogue: O / l, LSE
-      mbar_wait(&bars->o_full[h], oph);
+      mbar_wait_warp(&bars->o_full[h], oph);
       oph ^= 1;
       tc_fence_after();
       const bool valid = qi < tk.n_q;
@@ -339,10 +317,6 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
 }  // namespace fwd
 
 }  // namespace cad_dev
-
-namespace cad_dev {
-void cuda_check(cudaError_t e, const char* what);
-}
 
 extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k, const void* v,
                           void* o, float* lse, void* stream) {

@@ -63,50 +63,85 @@ void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads) 
   if (r != CUDA_SUCCESS) throw cad::CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
 }
 
+void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(heads)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(rows) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTile), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cad::CudaError("cuTensorMapEncodeTiled(rows) failed: " + std::to_string(int(r)));
+}
+
 static void build_units(cad_ca_plan& P) {
   const int hq = P.shape.h_q, hkv = P.shape.h_kv, group = hq / hkv;
   const int per_unit = (group % 2 == 0) ? 2 : 1;  // query heads sharing one KV tile stream
-  for (int32_t t = 0; t < static_cast<int32_t>(P.tasks.size()); ++t) {
+  const int n_tasks = static_cast<int>(P.tasks.size());
+  for (int32_t t = 0; t < n_tasks; ++t) {
     const DevTask& tk = P.tasks[t];
     const int shift = tk.kv_len - tk.n_q;
     const int n_qt = (tk.n_q + kTile - 1) / kTile;
-    const int n_kt = (tk.kv_len + kTile - 1) / kTile;
     for (int i = 0; i < n_qt; ++i) {
       const int last_pos = shift + std::min(tk.n_q, (i + 1) * kTile) - 1;
       const int n_kv = last_pos / kTile + 1;
-      for (int hk = 0; hk < hkv; ++hk)
-        for (int g = 0; g < group; g += per_unit) {
-          FwdUnit u;
-          u.task = t;
-          u.tile = i;
-          u.head0 = static_cast<int16_t>(hk * group + g);
-          u.nh = static_cast<int16_t>(per_unit);
-          u.n_kv = n_kv;
-          P.fwd_units.push_back(u);
-        }
+      for (int hk = 0; hk < hkv; ++hk) {
+        for (int g = 0; g < group; g += per_unit)
+          P.fwd_units.push_back({t, i, static_cast<int16_t>(hk * group + g), static_cast<int16_t>(per_unit), n_kv});
+        for (int g = 0; g < group; ++g)
+          P.dq_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 1, n_kv});
+      }
     }
+  }
+  // KV groups: tasks sharing kv_off. Groups must own disjoint KV rows and
+  // tasks disjoint Q rows, otherwise the backward's plain (non-atomic)
+  // stores would race.
+  std::vector<int> order(n_tasks);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return P.tasks[a].kv_off < P.tasks[b].kv_off; });
+  std::vector<std::pair<int, int>> qspans;
+  for (const DevTask& t : P.tasks) qspans.push_back({t.q_off, t.q_off + t.n_q});
+  std::sort(qspans.begin(), qspans.end());
+  for (size_t i = 1; i < qspans.size(); ++i)
+    if (qspans[i].first < qspans[i - 1].second) throw cad::DomainError("CA tasks overlap in Q rows");
+  int prev_end = -1;
+  for (size_t a = 0; a < order.size();) {
+    size_t b = a;
+    int kv_off = P.tasks[order[a]].kv_off, kv_end = kv_off;
+    while (b < order.size() && P.tasks[order[b]].kv_off == kv_off) {
+      kv_end = std::max(kv_end, P.tasks[order[b]].kv_off + P.tasks[order[b]].kv_len);
+      ++b;
+    }
+    if (kv_off < prev_end) throw cad::DomainError("CA task KV ranges overlap without sharing kv_off");
+    prev_end = kv_end;
+    const int n_kt = (kv_end - kv_off + kTile - 1) / kTile;
     for (int j = 0; j < n_kt; ++j) {
-      // First q row whose position reaches key j*128: shift + qi >= j*128.
-      const int q_first = std::max(0, j * kTile - shift);
-      if (q_first >= tk.n_q) continue;  // unreachable for kv_len >= n_q, kept for safety
+      const int32_t seg_begin = static_cast<int32_t>(P.kv_segs.size());
+      int32_t len = 0;
+      for (size_t x = a; x < b; ++x) {
+        const DevTask& tk = P.tasks[order[x]];
+        const int shift = tk.kv_len - tk.n_q;
+        const int q_first = std::max(0, j * kTile - shift);  // first query that sees key j*128
+        if (q_first >= tk.n_q) continue;
+        const int n_qt = (tk.n_q + kTile - 1) / kTile;
+        P.kv_segs.push_back({order[x], q_first / kTile, n_qt});
+        len += n_qt - q_first / kTile;
+      }
+      const int32_t seg_end = static_cast<int32_t>(P.kv_segs.size());
+      if (len == 0) continue;
       for (int hk = 0; hk < hkv; ++hk)
-        for (int g = 0; g < group; g += per_unit) {
-          BwdUnit u;
-          u.task = t;
-          u.tile = j;
-          u.head0 = static_cast<int16_t>(hk * group + g);
-          u.nh = static_cast<int16_t>(per_unit);
-          u.q_lo = q_first / kTile;
-          u.n_qt = n_qt;
-          P.bwd_units.push_back(u);
-        }
+        P.kv_units.push_back({kv_off, kv_end, j, static_cast<int16_t>(hk), 0, seg_begin, seg_end, len * group});
     }
+    a = b;
   }
   std::stable_sort(P.fwd_units.begin(), P.fwd_units.end(),
                    [](const FwdUnit& a, const FwdUnit& b) { return a.n_kv > b.n_kv; });
-  std::stable_sort(P.bwd_units.begin(), P.bwd_units.end(), [](const BwdUnit& a, const BwdUnit& b) {
-    return (a.n_qt - a.q_lo) > (b.n_qt - b.q_lo);
-  });
+  std::stable_sort(P.dq_units.begin(), P.dq_units.end(),
+                   [](const FwdUnit& a, const FwdUnit& b) { return a.n_kv > b.n_kv; });
+  std::stable_sort(P.kv_units.begin(), P.kv_units.end(),
+                   [](const KvUnit& a, const KvUnit& b) { return a.n_iter > b.n_iter; });
 }
 
 }  // namespace cad_dev
@@ -153,7 +188,9 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     };
     upload(P->tasks, &P->d_tasks);
     upload(P->fwd_units, &P->d_fwd);
-    upload(P->bwd_units, &P->d_bwd);
+    upload(P->dq_units, &P->d_dq);
+    upload(P->kv_units, &P->d_kv);
+    upload(P->kv_segs, &P->d_segs);
     *plan = P.release();
   });
 }
@@ -162,13 +199,14 @@ int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info) {
   return cad::guarded([&] {
     if (!plan || !info) throw cad::DomainError("null argument");
     info->n_fwd_units = static_cast<int64_t>(plan->fwd_units.size());
-    info->n_bwd_units = static_cast<int64_t>(plan->bwd_units.size());
+    info->n_bwd_units = static_cast<int64_t>(plan->kv_units.size() + plan->dq_units.size());
     info->causal_pairs = plan->pairs;
     const double base = double(plan->shape.head_dim) * double(plan->shape.h_q) * double(plan->pairs);
     info->fwd_flops = 4.0 * base;
     info->bwd_flops = 10.0 * base;
-    // dQ fp32 accumulator + delta = rowsum(dO*O) per (head, row)
-    info->workspace_bytes = size_t(plan->shape.q_rows) * plan->shape.h_q * (plan->shape.head_dim + 1) * 4;
+    // D = rowsum(dO * O) and log2-domain LSE per (head, row), fp32, rows
+    // padded to a multiple of 4 (16-byte TMA pitch)
+    info->workspace_bytes = size_t(2) * ((plan->shape.q_rows + 3) / 4 * 4) * plan->shape.h_q * 4;
   });
 }
 
@@ -177,7 +215,9 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     if (!plan) return;
     cudaFree(plan->d_tasks);
     cudaFree(plan->d_fwd);
-    cudaFree(plan->d_bwd);
+    cudaFree(plan->d_dq);
+    cudaFree(plan->d_kv);
+    cudaFree(plan->d_segs);
     delete plan;
   });
 }
