@@ -300,13 +300,28 @@ int cad_ca_plan_destroy(cad_ca_plan* plan);
 int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
                const void* v, void* o, float* lse, void* stream);
 
-/* Backward: dQ, dK, dV from Q, K, V, O, dO, LSE. dK/dV are accumulated
- * (+=) only if accumulate != 0, else overwritten; rows of tasks sharing a
- * KV prefix sum their contributions. workspace >= workspace_bytes. */
+/* Backward: dQ, dK, dV from Q, K, V, O, dO, LSE. Deterministic (no atomics).
+ * dQ rows of every task and dK/dV rows of every KV group (tasks sharing one
+ * kv_off, e.g. shards of one document) are overwritten; the group's rows
+ * receive the sum over all of its tasks. Tasks must have disjoint Q rows and
+ * groups disjoint KV rows (CAD_ERR_DOMAIN at plan creation otherwise).
+ * workspace >= workspace_bytes. */
 int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
                const void* v, const void* o, const float* lse, const void* dout,
                void* dq, void* dk, void* dv, void* workspace, size_t ws_bytes,
                void* stream);
+
+/* The backward's launches, separately: D = rowsum(dO*O) (+ log2 LSE) into the
+ * workspace, then dK/dV and dQ, which only depend on the workspace and may
+ * run on different streams once DELTA has completed. */
+#define CAD_BWD_DELTA 1
+#define CAD_BWD_DKDV 2
+#define CAD_BWD_DQ 4
+#define CAD_BWD_ALL 7
+int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const void* k,
+                     const void* v, const void* o, const float* lse,
+                     const void* dout, void* dq, void* dk, void* dv,
+                     void* workspace, size_t ws_bytes, int parts, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* Device: dispatch / return (replace layer_windows, P/src/sim.cpp:69-125)  */

@@ -122,6 +122,7 @@ SIGNATURES = {
     "cad_ca_plan_destroy": (C.c_int, [vp]),
     "cad_ca_fwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),  # plan q k v o lse stream
     "cad_ca_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]),
+    "cad_ca_bwd_parts": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int, vp]),
     "cad_comm_unique_id": (C.c_int, [P(u8)]),
     "cad_comm_init": (C.c_int, [P(u8), i32, i32, P(vp)]),
     "cad_comm_destroy": (C.c_int, [vp]),

@@ -19,6 +19,7 @@ from . import _native as N
 from ._native import check, lib
 
 HEAD_DIM = 128
+BWD_DELTA, BWD_DKDV, BWD_DQ, BWD_ALL = 1, 2, 4, 7
 
 
 @dataclass(frozen=True)
@@ -91,7 +92,7 @@ class CAPlan:
         return o, lse
 
     def backward(self, q, k, v, o, lse, do, dq=None, dk=None, dv=None, workspace=None,
-                 stream: Optional[torch.cuda.Stream] = None):
+                 stream: Optional[torch.cuda.Stream] = None, parts: int = BWD_ALL):
         if dq is None:
             dq = torch.empty_like(q)
         if dk is None:
@@ -100,8 +101,9 @@ class CAPlan:
             dv = torch.zeros_like(v)
         if workspace is None:
             workspace = torch.empty(max(1, self.workspace_bytes), dtype=torch.uint8, device=q.device)
-        check(lib().cad_ca_bwd(self._h, _need(q, "q"), _need(k, "k"), _need(v, "v"), _need(o, "o"),
-                               _need(lse, "lse", torch.float32), _need(do, "do"), _need(dq, "dq"),
-                               _need(dk, "dk"), _need(dv, "dv"), _need(workspace, "workspace", torch.uint8),
-                               workspace.numel(), _stream_ptr(stream)))
+        check(lib().cad_ca_bwd_parts(self._h, _need(q, "q"), _need(k, "k"), _need(v, "v"), _need(o, "o"),
+                                     _need(lse, "lse", torch.float32), _need(do, "do"), _need(dq, "dq"),
+                                     _need(dk, "dk"), _need(dv, "dv"),
+                                     _need(workspace, "workspace", torch.uint8), workspace.numel(),
+                                     parts, _stream_ptr(stream)))
         return dq, dk, dv

@@ -591,9 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
 }  // namespace bwd
 }  // namespace cad_dev
 
-extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k, const void* v,
-                          const void* o, const float* lse, const void* dout, void* dq, void* dk,
-                          void* dv, void* workspace, size_t ws_bytes, void* stream) {
+extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const void* k,
+                                const void* v, const void* o, const float* lse, const void* dout,
+                                void* dq, void* dk, void* dv, void* workspace, size_t ws_bytes,
+                                int parts, void* stream) {
   using namespace cad_dev;
   using namespace cad_dev::bwd;
   return cad::guarded([&] {
@@ -619,17 +620,19 @@ extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
       attr_set = true;
     }
     // 1. D = rowsum(dO * O)
-    int64_t rows = 0;
-    for (const DevTask& t : plan->tasks) rows += t.n_q;
-    const int64_t warps = rows * sh.h_q;
-    const int per_block = 8;
-    ca_delta_kernel<<<static_cast<unsigned>((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
-        plan->d_tasks, static_cast<int>(plan->tasks.size()), static_cast<const __nv_bfloat16*>(o),
-        static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, sh.h_q, sh.q_rows, pitch);
-    cuda_check(cudaGetLastError(), "ca_delta launch");
-    if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
+    if (parts & CAD_BWD_DELTA) {
+      int64_t rows = 0;
+      for (const DevTask& t : plan->tasks) rows += t.n_q;
+      const int64_t warps = rows * sh.h_q;
+      const int per_block = 8;
+      ca_delta_kernel<<<static_cast<unsigned>((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
+          plan->d_tasks, static_cast<int>(plan->tasks.size()), static_cast<const __nv_bfloat16*>(o),
+          static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, sh.h_q, sh.q_rows, pitch);
+      cuda_check(cudaGetLastError(), "ca_delta launch");
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
+    }
     // 2. dK, dV
-    if (!plan->kv_units.empty()) {
+    if ((parts & CAD_BWD_DKDV) && !plan->kv_units.empty()) {
       kv::Params p;
       make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
       make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
@@ -654,7 +657,7 @@ extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv");
     }
     // 3. dQ
-    {
+    if (parts & CAD_BWD_DQ) {
       dq::Params p;
       make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
       make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
@@ -677,4 +680,11 @@ extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq");
     }
   });
+}
+
+extern "C" int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k, const void* v,
+                          const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                          void* dv, void* workspace, size_t ws_bytes, void* stream) {
+  return cad_ca_bwd_parts(plan, q, k, v, o, lse, dout, dq, dk, dv, workspace, ws_bytes,
+                          CAD_BWD_ALL, stream);
 }
