@@ -5,7 +5,8 @@
 // Three launches, all deterministic (no atomics):
 //   1. ca_delta:   D[h][row] = sum_d dO * O (fp32).
 //   2. ca_bwd_dkdv: one unit per (KV group, kv tile, KV head). For every
-//      query head of the GQA group and every q tile that can see the kv tile:
+//      query head of the GQA group and every 64-row q sub-tile that can see
+//      the kv tile (two sub-tiles in flight, one per warpgroup):
 //        S^T = K Q^T, dP^T = V dO^T                        (tcgen05 -> TMEM)
 //        P^T = exp(S^T - LSE), dS^T = P^T (dP^T - D)      (2 warpgroups, bf16
 //                                                          written back to TMEM)
@@ -17,9 +18,9 @@
 // The dQ pass recomputes S and dP (7 tile GEMMs instead of 5) in exchange for
 // no fp32 dQ atomics and exact determinism.
 //
-// Both main kernels: 12 warps = softmax-like warpgroups 0 and 1 (columns
-// 0-63 and 64-127 of each 128x128 tile, thread = TMEM lane = tile row),
-// control warpgroup 2 (warp 8 TMA producer, warp 9 MMA issuer).
+// Both main kernels: 12 warps = elementwise warpgroups 0 and 1 (thread =
+// TMEM lane = tile row), control warpgroup 2 (warp 8 TMA producer, warp 9
+// MMA issuer).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -81,9 +82,9 @@ __device__ __forceinline__ void tmem_row_to_global(uint32_t taddr, float mul, __
 }
 
 // ============================================================== D = rowsum
-// One warp per (row, head): 128 bf16 of dO and O, lanes take 4 each. Also
-// re-lays the forward's LSE as log2-domain rows with a 16-byte-aligned pitch
-// so the dK/dV kernel can TMA both per q tile.
+// One warp per (row, head): 128 bf16 of dO and O, lanes take 4 each. Stores
+// -D and the forward's LSE as -LSE*log2(e) in [h_q][pitch] rows (negated so
+// the consumers fold them into one FFMA2/FADD2).
 __global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bfloat16* o,
                                 const __nv_bfloat16* dout, const float* lse, float* delta,
                                 float* lse2, int h_q, int64_t q_rows, int64_t pitch) {
@@ -111,8 +112,8 @@ __global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bf
 #pragma unroll
       for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (lane == 0) {
-        delta[int64_t(h) * pitch + row] = s;
-        lse2[int64_t(h) * pitch + row] = lse[int64_t(h) * q_rows + row] * kLog2e;
+        delta[int64_t(h) * pitch + row] = -s;
+        lse2[int64_t(h) * pitch + row] = -lse[int64_t(h) * q_rows + row] * kLog2e;
       }
       return;
     }
@@ -121,27 +122,37 @@ __global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bf
 }
 
 // ============================================================== dK / dV
+// Ping-pong over 64-row q sub-tiles: iteration i (a (head, task, sub-tile)
+// triple) uses TMEM buffer b = i & 1 and is handled by warpgroup b, so while
+// one warpgroup exponentiates sub-tile i the tensor core already computes
+// S^T/dP^T of sub-tile i+1 and the dV/dK updates of i-1.
+//   TMEM: buf b: S^T [128b, 128b+64)  dP^T [128b+64, 128b+128)
+//         dV [256,384)  dK [384,512)
+//   P^T / dS^T (bf16) overwrite the first 32 columns of S^T / dP^T.
 namespace kv {
 
+constexpr int kStages = 4;
+constexpr uint32_t kSubBytes = kSub * kHeadDim * 2;  // 16 KB
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
-constexpr uint32_t kQOff = 2 * kTileBytes;   // 2 stages
-constexpr uint32_t kDOOff = 4 * kTileBytes;  // 2 stages
-constexpr uint32_t kRowOff = 6 * kTileBytes; // [stage][LSE 128 | D 128] fp32
-constexpr uint32_t kBarOff = kRowOff + 4 * 512;
+constexpr uint32_t kQOff = 2 * kTileBytes;                  // kStages x 16 KB
+constexpr uint32_t kDOOff = kQOff + kStages * kSubBytes;    // kStages x 16 KB
+constexpr uint32_t kRowOff = kDOOff + kStages * kSubBytes;  // [stage][LSE 64 | D 64] fp32
+constexpr uint32_t kBarOff = kRowOff + kStages * 512;
 constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 
 struct Bars {
   uint64_t kv_full, kv_empty;
-  uint64_t in_full[2], in_empty[2];
-  uint64_t s_full, dp_full, p_full, ds_full, acc_full, acc_free;
+  uint64_t in_full[kStages], in_empty[kStages];
+  uint64_t s_full[2], dp_full[2], p_full[2], ds_full[2];
+  uint64_t acc_full, acc_free;
   uint32_t tmem_base;
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_k, tm_v, tm_do;
-  const float* lse2;   // log2-domain LSE, [h_q][pitch]
-  const float* delta;  // [h_q][pitch]
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;  // q/do maps have 64-row boxes
+  const float* nlse2;   // -LSE * log2(e), [h_q][pitch]
+  const float* ndelta;  // -D, [h_q][pitch]
   int64_t pitch;
   const DevTask* tasks;
   const KvUnit* units;
@@ -155,7 +166,7 @@ struct Params {
   float scale_log2;  // softmax scale * log2(e)
 };
 
-// Iteration cursor over (head in group, segment, q tile) of one unit.
+// Iteration cursor over (head in group, segment, q sub-tile) of one unit.
 struct Cursor {
   int g, seg, qt;
   __device__ void start(const KvUnit& u, const KvSeg* segs) {
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
-  float* rows = reinterpret_cast<float*>(smem + kRowOff);  // [stage][lse 128 | d 128]
+  float* rows = reinterpret_cast<float*>(smem + kRowOff);  // [stage][lse 64 | d 64]
   const uint32_t sbase = smem_u32(smem);
   const uint32_t warp = warp_id(), lane = lane_id();
 
@@ -190,14 +201,16 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
     tma_prefetch(&p.tm_do);
     mbar_init(&bars->kv_full, 1);
     mbar_init(&bars->kv_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(&bars->in_full[i], 33);
       mbar_init(&bars->in_empty[i], 1);
     }
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->dp_full, 1);
-    mbar_init(&bars->p_full, 256);
-    mbar_init(&bars->ds_full, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->s_full[b], 1);
+      mbar_init(&bars->dp_full[b], 1);
+      mbar_init(&bars->p_full[b], 128);
+      mbar_init(&bars->ds_full[b], 128);
+    }
     mbar_init(&bars->acc_full, 1);
     mbar_init(&bars->acc_free, 256);
     fence_barrier_init();
@@ -207,16 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  // TMEM: S^T [0,128)  dP^T [128,256)  dV [256,384)  dK [384,512)
-  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+  const uint32_t tDV = tmem + 256, tDK = tmem + 384;
 
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 8) {
       // ---------------------------------------------------------- producer
-      // Lane 0 issues the TMA tile loads; the whole warp copies the tile's
-      // 128 LSE and 128 D values (arbitrary, unaligned row offsets) into
-      // shared memory with plain loads and arrives on in_full (count 33).
+      // Lane 0 issues the TMA tile loads; the whole warp copies the
+      // sub-tile's 64 -LSE and 64 -D values (arbitrary, unaligned row offsets,
+      // so cp.async rather than TMA) and each lane's async arrive lands on
+      // in_full when its copies have (count 1 + 32).
       uint32_t kv_it = 0, st = 0, ph = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const KvUnit un = p.units[u];
@@ -235,92 +248,101 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
           const DevTask tk = p.tasks[p.segs[c.seg].task];
           const int head = un.hk * p.group + c.g;
-          const int qrow = tk.q_off + c.qt * kTile;
+          const int qrow = tk.q_off + c.qt * kSub;
           mbar_wait(&bars->in_empty[st], ph ^ 1);
           if (lane == 0) {
-            mbar_expect_tx(&bars->in_full[st], 2 * kTileBytes);
-            uint8_t* q = smem + kQOff + st * kTileBytes;
-            uint8_t* d = smem + kDOOff + st * kTileBytes;
+            mbar_expect_tx(&bars->in_full[st], 2 * kSubBytes);
+            uint8_t* q = smem + kQOff + st * kSubBytes;
+            uint8_t* d = smem + kDOOff + st * kSubBytes;
             tma_load_3d(&p.tm_q, &bars->in_full[st], q, 0, qrow, head);
-            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kTileBytes / 2, 64, qrow, head);
+            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kSubBytes / 2, 64, qrow, head);
             tma_load_3d(&p.tm_do, &bars->in_full[st], d, 0, qrow, head);
-            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kTileBytes / 2, 64, qrow, head);
+            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kSubBytes / 2, 64, qrow, head);
           }
-          float* dst = rows + st * 256;
-          const int64_t hbase = int64_t(head) * p.pitch;
+          float* dst = rows + st * 128;
+          const float* nl = p.nlse2 + int64_t(head) * p.pitch;
+          const float* nd = p.ndelta + int64_t(head) * p.pitch;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < 2; ++k) {
             const int col = lane + 32 * k;
-            const int64_t rrow = int64_t(qrow) + col;
-            const bool in = rrow < p.pitch;
-            dst[col] = in ? p.lse2[hbase + rrow] : 0.f;
-            dst[128 + col] = in ? p.delta[hbase + rrow] : 0.f;
+            // rows past the buffer only feed masked columns: clamp the source
+            const int64_t rrow = min(int64_t(qrow) + col, p.pitch - 1);
+            cp_async4(dst + col, nl + rrow);
+            cp_async4(dst + 64 + col, nd + rrow);
           }
-          mbar_arrive(&bars->in_full[st]);
-          if (++st == 2) { st = 0; ph ^= 1; }
+          cp_async_arrive(&bars->in_full[st]);
+          if (++st == kStages) { st = 0; ph ^= 1; }
         }
       }
     } else if (warp == 9 && lane == 0) {
       // ---------------------------------------------------------- MMA
       uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0;
-      uint32_t p_ph = 0, ds_ph = 0;
+      uint32_t p_ph[2] = {0, 0}, ds_ph[2] = {0, 0};
+      const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const KvUnit un = p.units[u];
         const int n = un.n_iter;
         mbar_wait(&bars->kv_full, kv_it & 1);
         ++kv_it;
-        mbar_wait(&bars->in_full[st], ph);
-        tc_fence_after();
-        const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
-        uint32_t sQ = sbase + kQOff + st * kTileBytes, sDO = sbase + kDOOff + st * kTileBytes;
-        issue_qk(tS, sK, sQ);
-        umma_commit(&bars->s_full);
-        issue_qk(tDP, sV, sDO);
-        umma_commit(&bars->dp_full);
+        // stage of iteration i is (st + i) % kStages with parity flips at wrap
+        auto stage_of = [&](int i, uint32_t& s, uint32_t& par) {
+          const uint32_t lin = st + i;
+          s = lin % kStages;
+          par = ph ^ ((lin / kStages) & 1);
+        };
+        for (int i = 0; i < 2 && i < n; ++i) {
+          uint32_t s, par;
+          stage_of(i, s, par);
+          mbar_wait(&bars->in_full[s], par);
+          tc_fence_after();
+          issue_qk_n<kSub>(tmem + 128 * i, sK, sbase + kQOff + s * kSubBytes);
+          umma_commit(&bars->s_full[i]);
+          issue_qk_n<kSub>(tmem + 128 * i + 64, sV, sbase + kDOOff + s * kSubBytes);
+          umma_commit(&bars->dp_full[i]);
+        }
         for (int i = 0; i < n; ++i) {
-          const uint32_t cur_st = st;
-          mbar_wait(&bars->p_full, p_ph);
-          p_ph ^= 1;
+          const int b = i & 1;
+          uint32_t s, par;
+          stage_of(i, s, par);
+          const uint32_t tSb = tmem + 128 * b, tDPb = tSb + 64;
+          mbar_wait(&bars->p_full[b], p_ph[b]);
+          p_ph[b] ^= 1;
           if (i == 0) {
             mbar_wait(&bars->acc_free, (acc_it & 1) ^ 1);
             ++acc_it;
           }
           tc_fence_after();
-          issue_pv(tDV, tS, tS + 64, sDO, i > 0);  // dV += P^T dO
-          uint32_t nQ = 0, nDO = 0;
-          if (i + 1 < n) {
-            if (++st == 2) { st = 0; ph ^= 1; }
-            mbar_wait(&bars->in_full[st], ph);
-            tc_fence_after();
-            nQ = sbase + kQOff + st * kTileBytes;
-            nDO = sbase + kDOOff + st * kTileBytes;
-            issue_qk(tS, sK, nQ);  // S^T(i+1)
-            umma_commit(&bars->s_full);
-          }
-          mbar_wait(&bars->ds_full, ds_ph);
-          ds_ph ^= 1;
+          issue_pv_k<kSub>(tDV, tSb, sbase + kDOOff + s * kSubBytes, i > 0);  // dV += P^T dO
+          mbar_wait(&bars->ds_full[b], ds_ph[b]);
+          ds_ph[b] ^= 1;
           tc_fence_after();
-          issue_pv(tDK, tDP, tDP + 64, sQ, i > 0);  // dK += dS^T Q
-          umma_commit(&bars->in_empty[cur_st]);
-          if (i + 1 < n) {
-            issue_qk(tDP, sV, nDO);  // dP^T(i+1)
-            umma_commit(&bars->dp_full);
-            sQ = nQ;
-            sDO = nDO;
+          issue_pv_k<kSub>(tDK, tDPb, sbase + kQOff + s * kSubBytes, i > 0);  // dK += dS^T Q
+          umma_commit(&bars->in_empty[s]);
+          if (i + 2 < n) {
+            uint32_t s2, par2;
+            stage_of(i + 2, s2, par2);
+            mbar_wait(&bars->in_full[s2], par2);
+            tc_fence_after();
+            issue_qk_n<kSub>(tSb, sK, sbase + kQOff + s2 * kSubBytes);
+            umma_commit(&bars->s_full[b]);
+            issue_qk_n<kSub>(tDPb, sV, sbase + kDOOff + s2 * kSubBytes);
+            umma_commit(&bars->dp_full[b]);
           }
         }
         umma_commit(&bars->acc_full);
         umma_commit(&bars->kv_empty);
-        if (++st == 2) { st = 0; ph ^= 1; }
+        const uint32_t lin = st + n;
+        st = lin % kStages;
+        ph ^= (lin / kStages) & 1;
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------------------ elementwise
-    const int w = warp >> 2;                    // column half: q cols [64w, 64w+64)
+    const int wg = warp >> 2;                   // handles iterations i with i % 2 == wg
     const uint32_t r = (warp & 3) * 32 + lane;  // kv row within the tile
     const uint32_t lsel = ((warp & 3) * 32) << 16;
-    const int c0 = 64 * w;
+    const uint32_t tSb = tmem + lsel + 128 * wg, tDPb = tSb + 64;
     uint32_t st = 0, ph = 0, s_ph = 0, dp_ph = 0, acc_ph = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const KvUnit un = p.units[u];
@@ -328,46 +350,71 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       Cursor c;
       c.start(un, p.segs);
       for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
+        const uint32_t cur = st, cur_ph = ph;
+        if (++st == kStages) { st = 0; ph ^= 1; }
+        if ((i & 1) != wg) continue;
         const DevTask tk = p.tasks[p.segs[c.seg].task];
         const int shift = tk.kv_len - tk.n_q;
-        const int q0 = c.qt * kTile + c0;  // query index of this thread's column 0
-        mbar_wait_warp(&bars->in_full[st], ph);
-        const float* lse = rows + st * 256 + c0;
-        const float* dd = rows + st * 256 + 128 + c0;
-        if (++st == 2) { st = 0; ph ^= 1; }
-        mbar_wait_warp(&bars->s_full, s_ph);
+        const int q0 = c.qt * kSub;  // query index of column 0
+        mbar_wait_warp(&bars->in_full[cur], cur_ph);
+        const uint32_t s_nlse = smem_u32(rows + cur * 128), s_nd = s_nlse + 256;
+        mbar_wait_warp(&bars->s_full[wg], s_ph);
         s_ph ^= 1;
         tc_fence_after();
         float x[64];
-        load_row64(tS + lsel + c0, x);
-        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q
-        const int lo = kj - shift - q0;        // first visible column
-        const int hi = tk.n_q - q0;            // columns >= hi are padding
+        load_row64(tSb, x);
+        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q; the
+        // sub-tile is mask-free (CTA-uniform) when the last kv row of the tile
+        // is visible from column 0 and all 64 columns are real queries.
+        const int lo = kj - shift - q0;
+        const int hi = tk.n_q - q0;
+        const bool full = (un.tile * kTile + kTile - 1 - shift - q0) <= 0 && hi >= kSub;
+        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const float e = ex2(fmaf(x[k], p.scale_log2, -lse[k]));
-          x[k] = (k >= lo && k < hi) ? e : 0.f;
+        for (int k = 0; k < 64; k += 4) {
+          const float4 nl = lds4(s_nlse + 4 * k);
+          float a0, a1, a2, a3;
+          f2_split(ffma2(f2(x[k], x[k + 1]), sc2, f2(nl.x, nl.y)), a0, a1);
+          f2_split(ffma2(f2(x[k + 2], x[k + 3]), sc2, f2(nl.z, nl.w)), a2, a3);
+          x[k] = ex2(a0);
+          x[k + 1] = ex2(a1);
+          x[k + 2] = ex2(a2);
+          x[k + 3] = ex2(a3);
         }
-        store_bf16_64(tS + lsel + 32 * w * 2, x);  // P^T: WG0 -> cols [0,32), WG1 -> [64,96)
+        if (!full) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) x[k] = (k >= lo && k < hi) ? x[k] : 0.f;
+        }
+        store_bf16_64(tSb, x);  // P^T into the first 32 columns of S^T
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->p_full);
-        mbar_wait_warp(&bars->dp_full, dp_ph);
+        mbar_arrive(&bars->p_full[wg]);
+        mbar_wait_warp(&bars->dp_full[wg], dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
         float y[64];
-        load_row64(tDP + lsel + c0, y);
+        load_row64(tDPb, y);
 #pragma unroll
-        for (int k = 0; k < 64; ++k) y[k] = (k >= lo && k < hi) ? x[k] * (y[k] - dd[k]) : 0.f;
-        store_bf16_64(tDP + lsel + 32 * w * 2, y);  // dS^T
+        for (int k = 0; k < 64; k += 4) {
+          const float4 nd = lds4(s_nd + 4 * k);
+          f2_split(fmul2(f2(x[k], x[k + 1]), fadd2(f2(y[k], y[k + 1]), f2(nd.x, nd.y))), y[k], y[k + 1]);
+          f2_split(fmul2(f2(x[k + 2], x[k + 3]), fadd2(f2(y[k + 2], y[k + 3]), f2(nd.z, nd.w))), y[k + 2],
+                   y[k + 3]);
+        }
+        if (!full) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) y[k] = (k >= lo && k < hi) ? y[k] : 0.f;
+        }
+        store_bf16_64(tDPb, y);  // dS^T
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->ds_full);
+        mbar_arrive(&bars->ds_full[wg]);
       }
-      // ---- epilogue: this warpgroup stores d columns [c0, c0+64) of dV and dK
+      // ---- epilogue: warpgroup wg stores d columns [64wg, 64wg+64) of dV and dK
       mbar_wait_warp(&bars->acc_full, acc_ph);
       acc_ph ^= 1;
       tc_fence_after();
+      const int c0 = 64 * wg;
       const int row = un.kv_off + kj;
       const bool valid = row < un.kv_end;
       const int64_t off = (int64_t(row) * p.h_kv + un.hk) * kHeadDim + c0;
@@ -408,8 +455,8 @@ struct Params {
   int n_units;
   int group;
   int h_q;
-  const float* lse2;   // log2-domain LSE, [h_q][pitch]
-  const float* delta;  // [h_q][pitch]
+  const float* lse2;   // -LSE * log2(e), [h_q][pitch]
+  const float* delta;  // -D, [h_q][pitch]
   __nv_bfloat16* dq;
   int64_t pitch;
   float scale;
@@ -544,8 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
       const int qi = un.tile * kTile + r;
       const bool valid = qi < tk.n_q;
       const int64_t row = int64_t(tk.q_off) + qi;
-      const float lse2 = valid ? p.lse2[int64_t(un.head0) * p.pitch + row] : 0.f;
-      const float dd = valid ? p.delta[int64_t(un.head0) * p.pitch + row] : 0.f;
+      const float lse2 = valid ? -p.lse2[int64_t(un.head0) * p.pitch + row] : 0.f;
+      const float dd = valid ? -p.delta[int64_t(un.head0) * p.pitch + row] : 0.f;
       const int pos = valid ? shift + qi : -1;  // invalid rows see nothing
       for (int j = 0; j < un.n_kv; ++j) {
         mbar_wait_warp(&bars->s_full, s_ph);
@@ -634,12 +681,12 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
     // 2. dK, dV
     if ((parts & CAD_BWD_DKDV) && !plan->kv_units.empty()) {
       kv::Params p;
-      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
-      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q, kSub);
+      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q, kSub);
       make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
       make_tile_map(&p.tm_v, v, sh.kv_rows, sh.h_kv);
-      p.lse2 = lse2;
-      p.delta = delta;
+      p.nlse2 = lse2;
+      p.ndelta = delta;
       p.pitch = pitch;
       p.tasks = plan->d_tasks;
       p.units = plan->d_kv;

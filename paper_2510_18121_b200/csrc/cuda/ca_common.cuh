@@ -30,11 +30,13 @@ struct FwdUnit {
   int32_t n_kv;
 };
 
+constexpr int kSub = 64;  // q sub-tile rows of the dK/dV kernel
+
 // dK/dV work unit: kv tile `tile` of a KV group (the tasks sharing one KV
 // row range [kv_off, kv_end), e.g. the shards of one document on this
 // server) for KV head hk. It walks, for every query head of hk's GQA group,
-// the segments seg_begin..seg_end-1: (task, q tiles qt_lo..qt_hi-1) that
-// can see the tile. One unit owns its dK/dV rows, so no reduction across
+// the segments seg_begin..seg_end-1: (task, 64-row q sub-tiles
+// qt_lo..qt_hi-1) that can see the tile. One unit owns its dK/dV rows, so no reduction across
 // units is needed.
 struct KvUnit {
   int32_t kv_off, kv_end, tile;
@@ -70,7 +72,7 @@ namespace cad_dev {
 // 3-D tiled map over a packed [rows][heads][128] bf16 buffer: box of
 // 64 d-values x 128 rows x 1 head, 128-byte swizzle. A 128x128 tile is two
 // boxes (d 0-63 and 64-127), landing as two 16 KB K-major SW128 planes.
-void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
+void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, int box_rows = kTile);
 // 2-D map over a [heads][rows] fp32 buffer (LSE, D): box of 128 rows x 1 head.
 void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
 void cuda_check(cudaError_t e, const char* what);

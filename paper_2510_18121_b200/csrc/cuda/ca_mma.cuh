@@ -41,4 +41,31 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t a_lo, uint32_
   }
 }
 
+// D = A B^T with a 128-row A tile and an N-row B tile (N = 64 or 128),
+// K = 128 (d). Each operand is two SW128 planes of 64 d-values; a plane of
+// an R-row tile is R*128 bytes.
+template <int N>
+__device__ __forceinline__ void issue_qk_n(uint32_t d_tmem, uint32_t a_smem, uint32_t b_smem) {
+  constexpr uint32_t idesc = idesc_bf16(128, N, false, false);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t kin = (k & 3) * 32;
+    umma_ss(d_tmem, sw128_desc(a_smem + (k >> 2) * (kTileBytes / 2) + kin, 16, 1024),
+            sw128_desc(b_smem + (k >> 2) * (N * 128) + kin, 16, 1024), idesc, k > 0 ? 1u : 0u);
+  }
+}
+
+// D (+)= A B with K = KR rows of an MN-major B tile (KR x 128 d, two planes
+// of KR*128 bytes) and A (bf16, M=128 lanes) in TMEM columns a + 8k.
+template <int KR>
+__device__ __forceinline__ void issue_pv_k(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem,
+                                           bool accumulate) {
+  constexpr uint32_t idesc = idesc_bf16(128, 128, false, true);
+#pragma unroll
+  for (int k = 0; k < KR / 16; ++k) {
+    umma_ts(d_tmem, a_tmem + k * 8, sw128_desc(b_smem + k * 2048, KR * 128, 1024), idesc,
+            (accumulate || k > 0) ? 1u : 0u);
+  }
+}
+
 }  // namespace cad_dev

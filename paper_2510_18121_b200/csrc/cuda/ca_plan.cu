@@ -49,12 +49,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads) {
+void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, int box_rows) {
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(rows),
                               static_cast<cuuint64_t>(heads)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(heads) * kHeadDim * 2,
                                  static_cast<cuuint64_t>(kHeadDim) * 2};
-  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kTile), 1};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -125,9 +125,9 @@ static void build_units(cad_ca_plan& P) {
         const int shift = tk.kv_len - tk.n_q;
         const int q_first = std::max(0, j * kTile - shift);  // first query that sees key j*128
         if (q_first >= tk.n_q) continue;
-        const int n_qt = (tk.n_q + kTile - 1) / kTile;
-        P.kv_segs.push_back({order[x], q_first / kTile, n_qt});
-        len += n_qt - q_first / kTile;
+        const int n_qs = (tk.n_q + kSub - 1) / kSub;
+        P.kv_segs.push_back({order[x], q_first / kSub, n_qs});
+        len += n_qs - q_first / kSub;
       }
       const int32_t seg_end = static_cast<int32_t>(P.kv_segs.size());
       if (len == 0) continue;

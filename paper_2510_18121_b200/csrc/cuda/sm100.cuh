@@ -52,25 +52,37 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-// Blocking wait on the phase with the given parity. A wait that has not
-// completed after ~20 s of suspended polling traps instead of hanging the
-// GPU (a deadlock is a bug; the trap surfaces it as a launch error).
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Blocking wait on the phase with the given parity. try_wait without a
+// suspend-time hint (a hint compiles to a long NANOSLEEP and oversleeps the
+// barrier completion). A wait that has not completed after ~20 s traps
+// instead of hanging the GPU (a deadlock is a bug; the trap surfaces it).
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return done != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  uint32_t done = 0;
-  for (uint32_t tries = 0;; ++tries) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (tries > 20000) {
+  if (mbar_try(addr, parity)) return;
+  const uint64_t t0 = global_ns();
+  for (uint32_t tries = 1;; ++tries) {
+    if (mbar_try(addr, parity)) return;
+    if ((tries & 0xFFFu) == 0 && global_ns() - t0 > 20000000000ull) {
       if ((threadIdx.x & 31) == 0 || threadIdx.x >= 256)
-      printf("cad: mbarrier wait timeout block %d thread %d smem 0x%x parity %u dbg %x %x %x %x\n",
-             blockIdx.x, threadIdx.x, addr, parity CAD_DBG_ARGS);
+        printf("cad: mbarrier wait timeout block %d thread %d smem 0x%x parity %u dbg %x %x %x %x\n",
+               blockIdx.x, threadIdx.x, addr, parity CAD_DBG_ARGS);
       __trap();
     }
   }
@@ -116,6 +128,16 @@ __device__ __forceinline__ void tma_load_3d(const void* desc, uint64_t* bar, voi
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// 4-byte asynchronous global->shared copy (LDGSTS) and an mbarrier arrive
+// that fires when all of this thread's prior cp.async copies have landed
+// (.noinc: the arrive counts against the barrier's expected count).
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // ---------------------------------------------------------------- TMEM
@@ -239,6 +261,40 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// ---------------------------------------------------------------- f32x2
+// Packed FP32 pairs (sm_100a FFMA2/FADD2/FMUL2): two lanes of math per
+// instruction on the FMA pipe.
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float4 lds4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(saddr));
+  return v;
 }
 
 // Named barrier among `threads` threads (id 1..15; 0 is __syncthreads).
