@@ -319,8 +319,8 @@ def main():
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
-        from paper_2510_18121_b200 import dist_bench
-        dist_bench.run(args, METRIC, load_peaks)
+        import bench_dist
+        bench_dist.run(args, METRIC, load_peaks, ClockSampler)
         return
     single_gpu(args)
 

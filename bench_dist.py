@@ -1,0 +1,161 @@
+"""N>1 leg of bench.py (launched by torchrun, one process per GPU).
+
+Workload: BASELINE config 3 shape (Llama-3-8B CA, 32 Q / 8 KV heads), 65536
+tokens per GPU (512K at 8 GPUs), pretrain_upsampled documents (seed 1),
+placed sequentially; CA-tasks sharded by the bit-exact scheduler; per layer
+the Q/KV dispatch, CA fwd, O/LSE return, dO dispatch, CA bwd, dQ and dK/dV
+return run over NCCL all-to-allv with ping/pong halves (dispatch.py).
+Scaling is weak (fixed tokens per GPU). Times are CUDA events on the compute
+stream, max over ranks.
+"""
+import json
+import os
+import statistics
+
+import torch
+import torch.distributed as dist
+
+
+def _timed(fn, steps, stream):
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    st.record(stream)
+    for _ in range(steps):
+        fn()
+    en.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = st.elapsed_time(en) / steps
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item(), ms
+
+
+def run(args, metric, load_peaks, ClockSampler):
+    os.environ.setdefault("NCCL_MAX_NCHANNELS", os.environ.get("CAD_NCCL_CHANNELS", "8"))
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_18121_b200 import configs as CF
+    from paper_2510_18121_b200 import dispatch as D
+    from paper_2510_18121_b200 import scheduler as S
+
+    shape = CF.LLAMA8B
+    per_gpu = 65536
+    lengths = S.sample_batch(CF.length_dist("pretrain", 1), per_gpu * world)
+    lp = D.LayerPlan(lengths, world, rank, shape)
+    obj = [D.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = D.Comm(obj[0], rank, world)
+    reserve = int(os.environ.get("CAD_RESERVE_SMS", "8"))
+    dev = torch.device("cuda", local)
+    layer = D.DistCALayer(lp, comm, dev, reserve_sms=reserve)
+    H = lp.home_rows
+    g = torch.Generator(device=dev).manual_seed(rank)
+    bf = dict(device=dev, dtype=torch.bfloat16)
+    q = torch.randn(H, shape.h_q, 128, generator=g, **bf)
+    k = torch.randn(H, shape.h_kv, 128, generator=g, **bf)
+    v = torch.randn(H, shape.h_kv, 128, generator=g, **bf)
+    do = torch.randn(H, shape.h_q, 128, generator=g, **bf)
+    o = torch.empty_like(q)
+    lse = torch.empty(shape.h_q, H, device=dev)
+    dq = torch.empty_like(q)
+    dk_acc = torch.zeros(H, shape.h_kv, 128, device=dev)
+    dv_acc = torch.zeros_like(dk_acc)
+    dk = torch.empty_like(k)
+    dv = torch.empty_like(v)
+    comp = torch.cuda.current_stream(dev)
+
+    def step(mode="pingpong"):
+        layer.step(q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode=mode)
+        lib = D.lib()
+        lib.cad_f32_to_bf16(dk_acc.data_ptr(), dk_acc.numel(), dk.data_ptr(), comp.cuda_stream)
+        lib.cad_f32_to_bf16(dv_acc.data_ptr(), dv_acc.numel(), dv.data_ptr(), comp.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    layer.launches = 0
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, my_ms = _timed(step, args.steps, comp)
+    clk = clocks.stop()
+    launches = layer.launches + 2 * args.steps
+    ms_compute, my_compute = _timed(lambda: step("compute"), max(2, args.steps // 2), comp)
+    ms_comm, _ = _timed(lambda: step("comm"), max(2, args.steps // 2), comp)
+    ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)
+
+    # e2e: home inputs from pinned host memory, gradients back to host
+    hq_, hk_, hv_, hdo_ = (t.cpu().pin_memory() for t in (q, k, v, do))
+    hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (dq, dk, dv))
+
+    def e2e():
+        q.copy_(hq_, non_blocking=True)
+        k.copy_(hk_, non_blocking=True)
+        v.copy_(hv_, non_blocking=True)
+        do.copy_(hdo_, non_blocking=True)
+        step()
+        hdq.copy_(dq, non_blocking=True)
+        hdk.copy_(dk, non_blocking=True)
+        hdv.copy_(dv, non_blocking=True)
+
+    e2e()
+    ms_e2e, _ = _timed(e2e, max(2, args.steps // 2), comp)
+    h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_, hdo_)) * world
+    d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv)) * world
+
+    pairs = lp.server_pairs()
+    wire = sum(sum(hp.remote_send_bytes) for hp in lp.halves)
+    wire_fwd = sum(hp.remote_send_bytes[0] * 2 + hp.remote_send_bytes[1] for hp in lp.halves)
+    stats = torch.tensor([pairs, my_compute, wire, my_ms], dtype=torch.float64, device=dev)
+    allst = [torch.zeros_like(stats) for _ in range(world)]
+    dist.all_gather(allst, stats)
+    allst = torch.stack(allst).cpu().numpy()
+    if rank == 0:
+        peak, peak_sus, peak_kind = load_peaks()
+        total_pairs = allst[:, 0].sum()
+        flops = 14.0 * 128 * shape.h_q * total_pairs
+        value = flops / ms / 1e9
+        hidden = None
+        if ms_comm > 0:
+            hidden = max(0.0, min(1.0, 1.0 - (ms - ms_compute) / ms_comm))
+        naive_pairs = []
+        for r in range(world):
+            its = [it for it in lp.home_items if it.home_device == r]
+            naive_pairs.append(sum(S.exact_causal_pairs(it.q_end - it.q_begin, it.q_end) for it in its))
+        out = {
+            "metric": metric, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 3 shape: Llama-3-8B CA (32 Q / 8 KV), {per_gpu} tokens per GPU "
+                                   f"({per_gpu * world} total), pretrain_upsampled seed 1, scheduler-sharded, "
+                                   "NCCL all-to-allv dispatch/return, ping-pong halves, one layer fwd+bwd",
+                       "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
+                       "flops_per_step": flops, "l2": "inputs larger than L2",
+                       "parallelism": f"CA servers x{world} (scheduler sharding)",
+                       "reserve_sms_for_comm": int(os.environ.get("CAD_RESERVE_SMS", "8"))},
+            "per_gpu_tflops": value / world, "pct_bf16_peak": value / world / peak,
+            "tokens_per_s": per_gpu * world / (ms / 1e3),
+            "imbalance": {"max_over_mean_pairs": float(allst[:, 0].max() / allst[:, 0].mean()),
+                          "max_over_mean_ca_time": float(allst[:, 1].max() / allst[:, 1].mean()),
+                          "naive_max_over_mean_pairs": max(naive_pairs) / (sum(naive_pairs) / world)},
+            "comm": {"ms_compute_only": ms_compute, "ms_comm_only": ms_comm, "ms_serial": ms_serial,
+                     "ms_pingpong": ms, "hidden_fraction": hidden,
+                     "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
+                     "nvlink_gbs_per_gpu": float(allst[:, 2].max()) / (ms_comm / 1e3) / 1e9 if ms_comm else None,
+                     "ref_total_comm_bytes": lp.plan.total_comm_bytes},
+            "roofline": {"kernel": "ca fwd+bwd (4 launches per half)", "bound": "tensor",
+                         "achieved": flops / world / ms_compute / 1e9, "peak": peak, "unit": "TFLOP/s",
+                         "frac": flops / world / ms_compute / 1e9 / peak, "traffic": None, "peak_kind": peak_kind},
+            "cpu_baseline": None,
+            "e2e": {"value": flops / ms_e2e / 1e9, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(out))
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()

@@ -295,6 +295,9 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks,
                        const cad_ca_shape* shape, cad_ca_plan** plan);
 int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info);
 int cad_ca_plan_destroy(cad_ca_plan* plan);
+/* Caps the persistent CTAs of this plan's launches (0 = one per SM), e.g.
+ * to leave SMs to NCCL kernels that overlap the CA kernel. */
+int cad_ca_plan_set_max_ctas(cad_ca_plan* plan, int max_ctas);
 
 /* Forward: O = softmax(scale * Q K^T + causal mask) V, LSE per (head, row). */
 int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
@@ -327,6 +330,50 @@ int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const void* k,
 /* Device: dispatch / return (replace layer_windows, P/src/sim.cpp:69-125)  */
 /* ---------------------------------------------------------------------- */
 
+/* One layer's data movement for one rank (the real counterpart of
+ * device_plans_from_schedule + layer_windows, P/src/sim.cpp:69-157). Built
+ * from a schedule and the pre-schedule home items (cad_place_sequential
+ * output); all ranks build it deterministically. Two halves (ping = 0,
+ * pong = 1, the assign_halves split). Per half, four row exchanges: */
+#define CAD_XFER_Q 0      /* Q (and dO) rows: home -> server            */
+#define CAD_XFER_KV 1     /* K/V rows: owner -> server (KV once per doc) */
+#define CAD_XFER_O_RET 2  /* O/LSE (and dQ) rows: server -> home         */
+#define CAD_XFER_KV_RET 3 /* dK/dV partial rows: server -> owner (summed) */
+
+typedef struct cad_layer_plan cad_layer_plan;
+
+typedef struct cad_layer_half_info {
+  int64_t home_rows;  /* rows of this rank's home buffers */
+  int64_t q_rows;     /* rows of the server Q/O/dO buffers of the half */
+  int64_t kv_rows;    /* rows of the server K/V buffers of the half */
+  int64_t n_tasks;
+  const cad_ca_task* tasks;   /* server CA-tasks (plan for cad_ca_plan_create) */
+  const int64_t* task_index;  /* index into cad_plan_tasks() per server task */
+  int64_t remote_send_bytes[4]; /* bytes this rank puts on the wire per xfer */
+} cad_layer_half_info;
+
+/* Row lists of one exchange as seen by this rank: send_idx lists source
+ * rows grouped by destination peer (send_counts[p] each), recv_idx lists
+ * destination rows grouped by source peer. Peer == rank is a local copy. */
+typedef struct cad_xfer {
+  int64_t n_peers;
+  const int64_t* send_counts;
+  const int64_t* send_idx;
+  const int64_t* recv_counts;
+  const int64_t* recv_idx;
+  int64_t n_send;
+  int64_t n_recv;
+} cad_xfer;
+
+int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items,
+                          int64_t n_items, int32_t rank, int64_t q_row_bytes,
+                          int64_t kv_row_bytes, cad_layer_plan** out);
+int cad_layer_plan_info(const cad_layer_plan* lp, int32_t half,
+                        cad_layer_half_info* info);
+int cad_layer_plan_xfer(const cad_layer_plan* lp, int32_t half, int32_t which,
+                        cad_xfer* x);
+void cad_layer_plan_destroy(cad_layer_plan* lp);
+
 typedef struct cad_comm cad_comm; /* one NCCL communicator per GPU */
 
 #define CAD_UNIQUE_ID_BYTES 128
@@ -338,11 +385,24 @@ int cad_comm_destroy(cad_comm* comm);
 /* Row gather: dst[i] = src[idx[i]] for rows of row_bytes (16-byte multiple). */
 int cad_gather_rows(const void* src, const int64_t* idx_dev, int64_t n_rows,
                     int64_t row_bytes, void* dst, void* stream);
-/* Row scatter(-add): dst[idx[i]] (+)= src[i]; add uses fp32 rows. */
+/* Row scatter: dst[idx[i]] = src[i]. */
 int cad_scatter_rows(const void* src, const int64_t* idx_dev, int64_t n_rows,
                      int64_t row_bytes, void* dst, void* stream);
-int cad_scatter_add_f32(const float* src, const int64_t* idx_dev, int64_t n_rows,
-                        int64_t row_elems, float* dst, void* stream);
+/* Row scatter-add of bf16 rows into fp32 rows: dst[idx[i]] += src[i]
+ * (row_elems elements per row); rows may repeat (partials are summed). */
+int cad_scatter_add_bf16(const void* src, const int64_t* idx_dev,
+                         int64_t n_rows, int64_t row_elems, float* dst,
+                         void* stream);
+/* Column gather/scatter of a [heads][rows] fp32 matrix (LSE):
+ * dst[i][h] = src[h][idx[i]] and its inverse. */
+int cad_gather_cols_f32(const float* src, int64_t src_rows, int32_t heads,
+                        const int64_t* idx_dev, int64_t n, float* dst,
+                        void* stream);
+int cad_scatter_cols_f32(const float* src, const int64_t* idx_dev, int64_t n,
+                         int32_t heads, float* dst, int64_t dst_rows,
+                         void* stream);
+/* fp32 -> bf16 elementwise (dK/dV accumulators to output). */
+int cad_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 
 /* All-to-allv over the communicator (grouped ncclSend/ncclRecv), byte
  * counts and displacements per peer, on `stream`. */

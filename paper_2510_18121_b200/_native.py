@@ -88,6 +88,18 @@ class cad_ca_plan_info(C.Structure):
                 ("fwd_flops", f64), ("bwd_flops", f64), ("workspace_bytes", C.c_size_t)]
 
 
+class cad_layer_half_info(C.Structure):
+    _fields_ = [("home_rows", i64), ("q_rows", i64), ("kv_rows", i64), ("n_tasks", i64),
+                ("tasks", C.POINTER(cad_ca_task)), ("task_index", C.POINTER(i64)),
+                ("remote_send_bytes", i64 * 4)]
+
+
+class cad_xfer(C.Structure):
+    _fields_ = [("n_peers", i64), ("send_counts", C.POINTER(i64)), ("send_idx", C.POINTER(i64)),
+                ("recv_counts", C.POINTER(i64)), ("recv_idx", C.POINTER(i64)), ("n_send", i64),
+                ("n_recv", i64)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 
@@ -123,12 +135,20 @@ SIGNATURES = {
     "cad_ca_fwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),  # plan q k v o lse stream
     "cad_ca_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]),
     "cad_ca_bwd_parts": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int, vp]),
+    "cad_ca_plan_set_max_ctas": (C.c_int, [vp, C.c_int]),
+    "cad_layer_plan_create": (C.c_int, [vp, P(cad_item), i64, i32, i64, i64, P(vp)]),
+    "cad_layer_plan_info": (C.c_int, [vp, i32, P(cad_layer_half_info)]),
+    "cad_layer_plan_xfer": (C.c_int, [vp, i32, i32, P(cad_xfer)]),
+    "cad_layer_plan_destroy": (None, [vp]),
+    "cad_scatter_add_bf16": (C.c_int, [vp, vp, i64, i64, vp, vp]),
+    "cad_gather_cols_f32": (C.c_int, [vp, i64, i32, vp, i64, vp, vp]),
+    "cad_scatter_cols_f32": (C.c_int, [vp, vp, i64, i32, vp, i64, vp]),
+    "cad_f32_to_bf16": (C.c_int, [vp, i64, vp, vp]),
     "cad_comm_unique_id": (C.c_int, [P(u8)]),
     "cad_comm_init": (C.c_int, [P(u8), i32, i32, P(vp)]),
     "cad_comm_destroy": (C.c_int, [vp]),
     "cad_gather_rows": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "cad_scatter_rows": (C.c_int, [vp, vp, i64, i64, vp, vp]),
-    "cad_scatter_add_f32": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "cad_alltoallv": (C.c_int, [vp, vp, P(i64), P(i64), vp, P(i64), P(i64), vp]),
 }
 

@@ -313,18 +313,23 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           }
           tc_fence_after();
           issue_pv_k<kSub>(tDV, tSb, sbase + kDOOff + s * kSubBytes, i > 0);  // dV += P^T dO
-          mbar_wait(&bars->ds_full[b], ds_ph[b]);
-          ds_ph[b] ^= 1;
-          tc_fence_after();
-          issue_pv_k<kSub>(tDK, tDPb, sbase + kQOff + s * kSubBytes, i > 0);  // dK += dS^T Q
-          umma_commit(&bars->in_empty[s]);
-          if (i + 2 < n) {
-            uint32_t s2, par2;
+          // S^T(i+2) may overwrite buffer b as soon as dV(i) (which reads P^T
+          // there) is issued: tcgen05 MMAs execute in issue order.
+          uint32_t s2 = 0, par2 = 0;
+          const bool more = i + 2 < n;
+          if (more) {
             stage_of(i + 2, s2, par2);
             mbar_wait(&bars->in_full[s2], par2);
             tc_fence_after();
             issue_qk_n<kSub>(tSb, sK, sbase + kQOff + s2 * kSubBytes);
             umma_commit(&bars->s_full[b]);
+          }
+          mbar_wait(&bars->ds_full[b], ds_ph[b]);
+          ds_ph[b] ^= 1;
+          tc_fence_after();
+          issue_pv_k<kSub>(tDK, tDPb, sbase + kQOff + s * kSubBytes, i > 0);  // dK += dS^T Q
+          umma_commit(&bars->in_empty[s]);
+          if (more) {
             issue_qk_n<kSub>(tDPb, sV, sbase + kDOOff + s2 * kSubBytes);
             umma_commit(&bars->dp_full[b]);
           }
@@ -698,7 +703,7 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.dv = static_cast<__nv_bfloat16*>(dv);
       p.scale = sh.softmax_scale;
       p.scale_log2 = sh.softmax_scale * kLog2e;
-      const int grid = std::min<int>(p.n_units, plan->num_sms);
+      const int grid = plan->grid(p.n_units);
       kv::ca_bwd_dkdv_kernel<<<grid, kThreads, kv::kSmemBytes, s>>>(p);
       cuda_check(cudaGetLastError(), "ca_bwd_dkdv launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv");
@@ -721,7 +726,7 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.pitch = pitch;
       p.scale = sh.softmax_scale;
       p.scale_log2 = sh.softmax_scale * kLog2e;
-      const int grid = std::min<int>(p.n_units, plan->num_sms);
+      const int grid = plan->grid(p.n_units);
       dq::ca_bwd_dq_kernel<<<grid, kThreads, dq::kSmemBytes, s>>>(p);
       cuda_check(cudaGetLastError(), "ca_bwd_dq launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq");

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -65,6 +66,11 @@ struct cad_ca_plan {
   int64_t pairs = 0;
   int device = 0;
   int num_sms = 148;
+  int max_ctas = 0;  // 0: one persistent CTA per SM
+  int grid(int64_t units) const {
+    const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;
+    return static_cast<int>(std::min<int64_t>(units, cap));
+  }
 };
 
 namespace cad_dev {

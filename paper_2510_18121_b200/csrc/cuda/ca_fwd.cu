@@ -344,7 +344,7 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
                  "cudaFuncSetAttribute(fwd)");
       attr_set = true;
     }
-    const int grid = std::min<int>(p.n_units, plan->num_sms);
+    const int grid = plan->grid(p.n_units);
     fwd::ca_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(p);
     cuda_check(cudaGetLastError(), "ca_fwd launch");
   });

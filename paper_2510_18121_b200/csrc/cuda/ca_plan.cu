@@ -7,8 +7,9 @@
 // tiles 0..n_kv-1 (tiles entirely above the diagonal are never visited).
 // Backward: one unit per (task, 128-row kv tile, KV head, pair of query
 // heads); it walks q tiles from the first one that can see the kv tile.
-// Units are sorted by length, longest first, so the persistent CTAs'
-// strided walk ends with the short units (LPT).
+// Units are sorted by KV head, then by length, longest first, so the
+// persistent CTAs' strided walk shares L2-resident tiles and ends each head
+// with its short units (LPT).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -136,12 +137,20 @@ static void build_units(cad_ca_plan& P) {
     }
     a = b;
   }
-  std::stable_sort(P.fwd_units.begin(), P.fwd_units.end(),
-                   [](const FwdUnit& a, const FwdUnit& b) { return a.n_kv > b.n_kv; });
-  std::stable_sort(P.dq_units.begin(), P.dq_units.end(),
-                   [](const FwdUnit& a, const FwdUnit& b) { return a.n_kv > b.n_kv; });
-  std::stable_sort(P.kv_units.begin(), P.kv_units.end(),
-                   [](const KvUnit& a, const KvUnit& b) { return a.n_iter > b.n_iter; });
+  // Head-major, then longest first: the ~148 concurrently running CTAs work
+  // on the same KV head, so the K/V (fwd, dq) or Q/dO (dkdv) tiles they all
+  // stream stay L2-resident; within a head the strided walk is LPT.
+  std::stable_sort(P.fwd_units.begin(), P.fwd_units.end(), [group](const FwdUnit& a, const FwdUnit& b) {
+    const int ha = a.head0 / group, hb = b.head0 / group;
+    return ha != hb ? ha < hb : a.n_kv > b.n_kv;
+  });
+  std::stable_sort(P.dq_units.begin(), P.dq_units.end(), [group](const FwdUnit& a, const FwdUnit& b) {
+    const int ha = a.head0 / group, hb = b.head0 / group;
+    return ha != hb ? ha < hb : a.n_kv > b.n_kv;
+  });
+  std::stable_sort(P.kv_units.begin(), P.kv_units.end(), [](const KvUnit& a, const KvUnit& b) {
+    return a.hk != b.hk ? a.hk < b.hk : a.n_iter > b.n_iter;
+  });
 }
 
 }  // namespace cad_dev
@@ -207,6 +216,13 @@ int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info) {
     // D = rowsum(dO * O) and log2-domain LSE per (head, row), fp32, rows
     // padded to a multiple of 4 (16-byte TMA pitch)
     info->workspace_bytes = size_t(2) * ((plan->shape.q_rows + 3) / 4 * 4) * plan->shape.h_q * 4;
+  });
+}
+
+int cad_ca_plan_set_max_ctas(cad_ca_plan* plan, int max_ctas) {
+  return cad::guarded([&] {
+    if (!plan || max_ctas < 0) throw cad::DomainError("bad argument");
+    plan->max_ctas = max_ctas;
   });
 }
 

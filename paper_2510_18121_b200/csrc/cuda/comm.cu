@@ -1,0 +1,259 @@
+// Dispatch/return data movement: NCCL all-to-allv over NVLink (grouped
+// ncclSend/ncclRecv on a caller stream) and the row gather/scatter kernels
+// that pack per-peer send buffers and unpack received rows into the server
+// (or home) layouts of cad_layer_plan.
+//
+// NCCL is bound at run time (dlopen of libnccl.so.2): inside a process that
+// already runs torch.distributed this resolves to the NCCL torch loaded, so
+// both communicators share one library.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "../host/cad_status.hpp"
+#include "ca_common.cuh"
+
+namespace {
+
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGetErrorString) err = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.h = h;
+    n.get_id = reinterpret_cast<decltype(n.get_id)>(dlsym(h, "ncclGetUniqueId"));
+    n.init_rank = reinterpret_cast<decltype(n.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "ncclCommDestroy"));
+    n.group_start = reinterpret_cast<decltype(n.group_start)>(dlsym(h, "ncclGroupStart"));
+    n.group_end = reinterpret_cast<decltype(n.group_end)>(dlsym(h, "ncclGroupEnd"));
+    n.send = reinterpret_cast<decltype(n.send)>(dlsym(h, "ncclSend"));
+    n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(h, "ncclRecv"));
+    n.err = reinterpret_cast<decltype(n.err)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (!n.h || !n.get_id || !n.init_rank || !n.send || !n.recv)
+    throw cad::NcclError(std::string("libnccl.so.2 unavailable: ") + (dlerror() ? dlerror() : "?"));
+  return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw cad::NcclError(std::string(what) + ": " + nccl().err(r));
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, const int64_t* __restrict__ idx,
+                                   int64_t n, int64_t chunks, uint4* __restrict__ dst) {
+  const int64_t total = n * chunks;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / chunks, c = t - r * chunks;
+    dst[t] = src[idx[r] * chunks + c];
+  }
+}
+
+__global__ void scatter_rows_kernel(const uint4* __restrict__ src, const int64_t* __restrict__ idx,
+                                    int64_t n, int64_t chunks, uint4* __restrict__ dst) {
+  const int64_t total = n * chunks;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / chunks, c = t - r * chunks;
+    dst[idx[r] * chunks + c] = src[t];
+  }
+}
+
+// 8 bf16 per thread added into 8 fp32 (atomic: a row may repeat).
+__global__ void scatter_add_bf16_kernel(const uint4* __restrict__ src, const int64_t* __restrict__ idx,
+                                        int64_t n, int64_t chunks, float* __restrict__ dst) {
+  const int64_t total = n * chunks;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / chunks, c = t - r * chunks;
+    const uint4 v = src[t];
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float* d = dst + (idx[r] * chunks + c) * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(b[i]);
+      atomicAdd(d + 2 * i, f.x);
+      atomicAdd(d + 2 * i + 1, f.y);
+    }
+  }
+}
+
+__global__ void gather_cols_kernel(const float* __restrict__ src, int64_t src_rows, int heads,
+                                   const int64_t* __restrict__ idx, int64_t n, float* __restrict__ dst) {
+  const int64_t total = n * heads;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / heads, h = t - i * heads;
+    dst[t] = src[h * src_rows + idx[i]];
+  }
+}
+
+__global__ void scatter_cols_kernel(const float* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                    int heads, float* __restrict__ dst, int64_t dst_rows) {
+  const int64_t total = n * heads;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / heads, h = t - i * heads;
+    dst[h * dst_rows + idx[i]] = src[t];
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ src, int64_t n4, uint2* __restrict__ dst) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n4; t += int64_t(gridDim.x) * blockDim.x) {
+    const float4 f = src[t];
+    __nv_bfloat162 a = __floats2bfloat162_rn(f.x, f.y), b = __floats2bfloat162_rn(f.z, f.w);
+    uint2 o;
+    std::memcpy(&o.x, &a, 4);
+    std::memcpy(&o.y, &b, 4);
+    dst[t] = o;
+  }
+}
+
+unsigned blocks_for(int64_t work) {
+  const int64_t b = (work + 255) / 256;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16)));
+}
+
+}  // namespace
+
+struct cad_comm {
+  ncclComm_t comm = nullptr;
+  int32_t rank = 0, world = 1;
+};
+
+extern "C" {
+
+int cad_comm_unique_id(uint8_t id[CAD_UNIQUE_ID_BYTES]) {
+  return cad::guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == CAD_UNIQUE_ID_BYTES, "unique id size");
+    ncclUniqueId u;
+    nccl_check(nccl().get_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int cad_comm_init(const uint8_t id[CAD_UNIQUE_ID_BYTES], int32_t rank, int32_t world, cad_comm** comm) {
+  return cad::guarded([&] {
+    if (!id || !comm || world < 1 || rank < 0 || rank >= world) throw cad::DomainError("bad argument");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    auto c = std::make_unique<cad_comm>();
+    c->rank = rank;
+    c->world = world;
+    nccl_check(nccl().init_rank(&c->comm, world, u, rank), "ncclCommInitRank");
+    *comm = c.release();
+  });
+}
+
+int cad_comm_destroy(cad_comm* comm) {
+  return cad::guarded([&] {
+    if (!comm) return;
+    if (comm->comm) nccl_check(nccl().destroy(comm->comm), "ncclCommDestroy");
+    delete comm;
+  });
+}
+
+int cad_alltoallv(cad_comm* comm, const void* send, const int64_t* send_bytes, const int64_t* send_displ,
+                  void* recv, const int64_t* recv_bytes, const int64_t* recv_displ, void* stream) {
+  return cad::guarded([&] {
+    if (!comm || !send_bytes || !send_displ || !recv_bytes || !recv_displ) throw cad::DomainError("null argument");
+    const Nccl& n = nccl();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    nccl_check(n.group_start(), "ncclGroupStart");
+    for (int32_t p = 0; p < comm->world; ++p) {
+      if (send_bytes[p] > 0)
+        nccl_check(n.send(static_cast<const char*>(send) + send_displ[p], static_cast<size_t>(send_bytes[p]), ncclUint8,
+                          p, comm->comm, s),
+                   "ncclSend");
+      if (recv_bytes[p] > 0)
+        nccl_check(n.recv(static_cast<char*>(recv) + recv_displ[p], static_cast<size_t>(recv_bytes[p]), ncclUint8, p,
+                          comm->comm, s),
+                   "ncclRecv");
+    }
+    nccl_check(n.group_end(), "ncclGroupEnd");
+  });
+}
+
+int cad_gather_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !idx || !dst || row_bytes % 16) throw cad::DomainError("bad gather arguments");
+    const int64_t chunks = row_bytes / 16;
+    gather_rows_kernel<<<blocks_for(n * chunks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(src), idx, n, chunks, static_cast<uint4*>(dst));
+    cad_dev::cuda_check(cudaGetLastError(), "gather_rows");
+  });
+}
+
+int cad_scatter_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes, void* dst, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !idx || !dst || row_bytes % 16) throw cad::DomainError("bad scatter arguments");
+    const int64_t chunks = row_bytes / 16;
+    scatter_rows_kernel<<<blocks_for(n * chunks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(src), idx, n, chunks, static_cast<uint4*>(dst));
+    cad_dev::cuda_check(cudaGetLastError(), "scatter_rows");
+  });
+}
+
+int cad_scatter_add_bf16(const void* src, const int64_t* idx, int64_t n, int64_t row_elems, float* dst,
+                         void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !idx || !dst || row_elems % 8) throw cad::DomainError("bad scatter-add arguments");
+    const int64_t chunks = row_elems / 8;
+    scatter_add_bf16_kernel<<<blocks_for(n * chunks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(src), idx, n, chunks, dst);
+    cad_dev::cuda_check(cudaGetLastError(), "scatter_add_bf16");
+  });
+}
+
+int cad_gather_cols_f32(const float* src, int64_t src_rows, int32_t heads, const int64_t* idx, int64_t n, float* dst,
+                        void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !idx || !dst) throw cad::DomainError("null argument");
+    gather_cols_kernel<<<blocks_for(n * heads), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, src_rows, heads,
+                                                                                               idx, n, dst);
+    cad_dev::cuda_check(cudaGetLastError(), "gather_cols");
+  });
+}
+
+int cad_scatter_cols_f32(const float* src, const int64_t* idx, int64_t n, int32_t heads, float* dst,
+                         int64_t dst_rows, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !idx || !dst) throw cad::DomainError("null argument");
+    scatter_cols_kernel<<<blocks_for(n * heads), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, idx, n, heads,
+                                                                                                dst, dst_rows);
+    cad_dev::cuda_check(cudaGetLastError(), "scatter_cols");
+  });
+}
+
+int cad_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!src || !dst || n % 4) throw cad::DomainError("bad conversion arguments");
+    f32_to_bf16_kernel<<<blocks_for(n / 4), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const float4*>(src), n / 4, static_cast<uint2*>(dst));
+    cad_dev::cuda_check(cudaGetLastError(), "f32_to_bf16");
+  });
+}
+
+}  // extern "C"

@@ -89,6 +89,9 @@ cad_plan* wrap(cad::Plan&& p) {
 
 }  // namespace
 
+const cad::Plan& cad_plan_ref(const cad_plan* p) { return p->plan; }
+const std::vector<cad::DevicePlan>& cad_plan_devices(const cad_plan* p) { return p->devices; }
+
 extern "C" {
 
 const char* cad_last_error(void) { return cad::last_error().c_str(); }

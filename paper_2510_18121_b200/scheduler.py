@@ -229,7 +229,7 @@ def propose_migration(source: ServerLoad, dest: ServerLoad, item: Item, target: 
                              out.v_comm, out.priority, bool(out.whole_item))
 
 
-def _unwrap_plan(h: C.c_void_p) -> SchedulePlan:
+def _unwrap_plan(h: C.c_void_p, free: bool = True) -> SchedulePlan:
     L = lib()
     try:
         st = N.cad_plan_stats()
@@ -264,13 +264,36 @@ def _unwrap_plan(h: C.c_void_p) -> SchedulePlan:
                             bool(st.tolerance_met), st.migrations, st.splits, st.rejected_small,
                             buf.value.decode(), devices)
     finally:
-        L.cad_plan_free(h)
+        if free:
+            L.cad_plan_free(h)
 
 
 def schedule(items: Sequence[Item], n_servers: int, cfg: SchedulerConfig) -> SchedulePlan:
     h = C.c_void_p()
     check(lib().cad_schedule(_items_array(items), len(items), n_servers, C.byref(cfg.to_c()), C.byref(h)))
     return _unwrap_plan(h)
+
+
+class PlanHandle:
+    """A live cad_plan (for consumers of the C-ABI such as cad_layer_plan);
+    .plan is its Python mirror."""
+
+    def __init__(self, items: Sequence[Item], n_servers: int, cfg: SchedulerConfig):
+        self.h = C.c_void_p()
+        check(lib().cad_schedule(_items_array(items), len(items), n_servers, C.byref(cfg.to_c()),
+                                 C.byref(self.h)))
+        self.plan = _unwrap_plan(self.h, free=False)
+
+    def close(self):
+        if self.h:
+            lib().cad_plan_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def schedule_pp_tick(per_stage_items: Sequence[Sequence[Item]], n_servers: int,

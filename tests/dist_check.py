@@ -1,0 +1,78 @@
+"""torchrun script: the distributed CA layer (NCCL dispatch/return, ping-pong)
+against the same batch computed whole on one GPU. Prints one JSON line of max
+errors per rank and exits non-zero on a mismatch.
+    torchrun --nproc-per-node 2 tests/dist_check.py [tokens_per_gpu]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import torch.distributed as dist
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_18121_b200 import configs as CF
+    from paper_2510_18121_b200 import dispatch as D
+    from paper_2510_18121_b200 import scheduler as S
+    from paper_2510_18121_b200.ca import CAPlan, CATaskRows
+    per = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+    shape = CF.Shape("check", 8, 2)
+    lengths = S.sample_batch(CF.length_dist("pretrain", 3, max_doc_len=per * world), per * world)
+    lp = D.LayerPlan(lengths, world, rank, shape)
+    obj = [D.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = D.Comm(obj[0], rank, world)
+    dev = torch.device("cuda", local)
+    layer = D.DistCALayer(lp, comm, dev, reserve_sms=8)
+    T = sum(lengths)
+    g = torch.Generator().manual_seed(5)
+    full = {n: torch.randn(T, h, 128, generator=g).to(torch.bfloat16)
+            for n, h in (("q", shape.h_q), ("k", shape.h_kv), ("v", shape.h_kv), ("do", shape.h_q))}
+    starts = [0]
+    for l in lengths[:-1]:
+        starts.append(starts[-1] + l)
+    mine = [it for it in lp.home_items if it.home_device == rank]
+    rows = torch.cat([torch.arange(starts[it.doc] + it.q_begin, starts[it.doc] + it.q_end) for it in mine])
+    home = {n: t[rows].contiguous().to(dev) for n, t in full.items()}
+    H = lp.home_rows
+    o = torch.empty_like(home["q"])
+    lse = torch.empty(shape.h_q, H, device=dev)
+    dq = torch.empty_like(home["q"])
+    dk_acc = torch.zeros(H, shape.h_kv, 128, device=dev)
+    dv_acc = torch.zeros_like(dk_acc)
+    for mode in ("pingpong", "serial"):
+        layer.step(home["q"], home["k"], home["v"], home["do"], o, lse, dq, dk_acc, dv_acc, mode=mode)
+    torch.cuda.synchronize()
+    # whole batch on this GPU
+    tasks = [CATaskRows(s, l, s, l) for s, l in zip(starts, lengths)]
+    plan = CAPlan(tasks, shape.h_q, shape.h_kv, T, T)
+    fq, fk, fv, fdo = (full[n].to(dev) for n in ("q", "k", "v", "do"))
+    ro, rlse = plan.forward(fq, fk, fv)
+    rdq, rdk, rdv = plan.backward(fq, fk, fv, ro, rlse, fdo)
+    torch.cuda.synchronize()
+    rows_d = rows.to(dev)
+    err = {
+        "o": (o.float() - ro[rows_d].float()).abs().max().item(),
+        "lse": (lse - rlse[:, rows_d]).abs().max().item(),
+        "dq": (dq.float() - rdq[rows_d].float()).abs().max().item(),
+        "dk": (dk_acc - rdk[rows_d].float()).abs().max().item(),
+        "dv": (dv_acc - rdv[rows_d].float()).abs().max().item(),
+        "migrations": lp.plan.migrations, "rank": rank,
+    }
+    scale = {"dq": rdq.float().abs().max().item(), "dk": rdk.float().abs().max().item(),
+             "dv": rdv.float().abs().max().item()}
+    ok = err["o"] <= 2e-2 and err["lse"] <= 1e-3 and all(err[k] <= 3e-2 * max(1, scale[k]) for k in scale)
+    print(json.dumps({**err, "ok": ok}), flush=True)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
