@@ -286,38 +286,41 @@ class DistCALayer:
         start = ev()
         start.record(comp)
         comm.wait_event(start)
-        ready = []
+        # comm stream: D(0) D(1) dO(0) dO(1) | R(0) R(1) | BR(0) BR(1)
+        # compute:            F(0) F(1)        B(0) B(1)
+        # so R(h) hides under F(1-h)/B(0), dO dispatch under F, BR(0) under B(1);
+        # only D(0) and BR(1) are exposed (the reference's ping-pong windows,
+        # P/src/sim.cpp:69-72, for a CA-only layer).
+        ready_f, ready_b = [], []
         for h in (0, 1):
             self.dispatch_fwd(h, q, k, v, comm)
             e = ev()
             e.record(comm)
-            ready.append(e)
-        done = []
-        for h in (0, 1):
-            comp.wait_event(ready[h])
-            self.ca_fwd(h, comp)
-            e = ev()
-            e.record(comp)
-            done.append(e)
-        for h in (0, 1):
-            comm.wait_event(done[h])
-            self.return_fwd(h, o, lse, comm)
-        # backward
-        ready = []
+            ready_f.append(e)
         for h in (0, 1):
             self.dispatch_bwd(h, do, comm)
             e = ev()
             e.record(comm)
-            ready.append(e)
-        done = []
+            ready_b.append(e)
+        done_f = []
         for h in (0, 1):
-            comp.wait_event(ready[h])
+            comp.wait_event(ready_f[h])
+            self.ca_fwd(h, comp)
+            e = ev()
+            e.record(comp)
+            done_f.append(e)
+        for h in (0, 1):
+            comm.wait_event(done_f[h])
+            self.return_fwd(h, o, lse, comm)
+        done_b = []
+        for h in (0, 1):
+            comp.wait_event(ready_b[h])
             self.ca_bwd(h, comp)
             e = ev()
             e.record(comp)
-            done.append(e)
+            done_b.append(e)
         for h in (0, 1):
-            comm.wait_event(done[h])
+            comm.wait_event(done_b[h])
             self.return_bwd(h, dq, dk_acc, dv_acc, comm)
         fin = ev()
         fin.record(comm)
