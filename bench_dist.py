@@ -50,7 +50,8 @@ def run(args, metric, load_peaks, ClockSampler):
     obj = [D.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = D.Comm(obj[0], rank, world)
-    reserve = int(os.environ.get("CAD_RESERVE_SMS", "8"))
+    transport = os.environ.get("CAD_TRANSPORT", "ce")
+    reserve = int(os.environ.get("CAD_RESERVE_SMS", "0" if transport == "ce" else "8"))
     dev = torch.device("cuda", local)
     layer = D.DistCALayer(lp, comm, dev, reserve_sms=reserve)
     H = lp.home_rows
@@ -68,6 +69,8 @@ def run(args, metric, load_peaks, ClockSampler):
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)
     comp = torch.cuda.current_stream(dev)
+    if transport == "ce":
+        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq)
 
     def step(mode="pingpong"):
         layer.step(q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode=mode)
@@ -78,14 +81,19 @@ def run(args, metric, load_peaks, ClockSampler):
     for _ in range(args.warmup):
         step()
     layer.launches = 0
+    if layer.ce is not None:
+        layer.ce.launches = 0
     clocks = ClockSampler(local)
     clocks.start()
     ms, my_ms = _timed(step, args.steps, comp)
     clk = clocks.stop()
-    launches = layer.launches + 2 * args.steps
+    launches = layer.launches + (layer.ce.launches if layer.ce is not None else 0) + 2 * args.steps
     ms_compute, my_compute = _timed(lambda: step("compute"), max(2, args.steps // 2), comp)
     ms_comm, _ = _timed(lambda: step("comm"), max(2, args.steps // 2), comp)
-    ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)
+    ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)  # NCCL, no overlap
+    ms_signal = None
+    if layer.ce is not None:
+        ms_signal, _ = _timed(lambda: step("signal"), max(2, args.steps // 2), comp)
 
     # e2e: home inputs from pinned host memory, gradients back to host
     hq_, hk_, hv_, hdo_ = (t.cpu().pin_memory() for t in (q, k, v, do))
@@ -118,9 +126,12 @@ def run(args, metric, load_peaks, ClockSampler):
         total_pairs = allst[:, 0].sum()
         flops = 14.0 * 128 * shape.h_q * total_pairs
         value = flops / ms / 1e9
+        # hidden = 1 - (T_pingpong - T_signal) / T_comm_only (the
+        # reference's signal/ping-pong modes, P/tests/acceptance.cpp:272-290)
         hidden = None
+        base = ms_signal if ms_signal is not None else ms_compute
         if ms_comm > 0:
-            hidden = max(0.0, min(1.0, 1.0 - (ms - ms_compute) / ms_comm))
+            hidden = max(0.0, min(1.0, 1.0 - (ms - base) / ms_comm))
         naive_pairs = []
         for r in range(world):
             its = [it for it in lp.home_items if it.home_device == r]
@@ -131,17 +142,18 @@ def run(args, metric, load_peaks, ClockSampler):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"BASELINE config 3 shape: Llama-3-8B CA (32 Q / 8 KV), {per_gpu} tokens per GPU "
                                    f"({per_gpu * world} total), pretrain_upsampled seed 1, scheduler-sharded, "
-                                   "NCCL all-to-allv dispatch/return, ping-pong halves, one layer fwd+bwd",
+                                   f"{'copy-engine (CUDA IPC) pushes' if transport == 'ce' else 'NCCL all-to-allv'} dispatch/return, "
+                                   "ping-pong halves, one layer fwd+bwd",
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
                        "parallelism": f"CA servers x{world} (scheduler sharding)",
-                       "reserve_sms_for_comm": int(os.environ.get("CAD_RESERVE_SMS", "8"))},
+                       "transport": transport, "reserve_sms_for_comm": reserve},
             "per_gpu_tflops": value / world, "pct_bf16_peak": value / world / peak,
             "tokens_per_s": per_gpu * world / (ms / 1e3),
             "imbalance": {"max_over_mean_pairs": float(allst[:, 0].max() / allst[:, 0].mean()),
                           "max_over_mean_ca_time": float(allst[:, 1].max() / allst[:, 1].mean()),
                           "naive_max_over_mean_pairs": max(naive_pairs) / (sum(naive_pairs) / world)},
-            "comm": {"ms_compute_only": ms_compute, "ms_comm_only": ms_comm, "ms_serial": ms_serial,
+            "comm": {"ms_compute_only": ms_compute, "ms_signal": ms_signal, "ms_comm_only": ms_comm, "ms_serial_nccl": ms_serial,
                      "ms_pingpong": ms, "hidden_fraction": hidden,
                      "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
                      "nvlink_gbs_per_gpu": float(allst[:, 2].max()) / (ms_comm / 1e3) / 1e9 if ms_comm else None,

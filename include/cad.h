@@ -404,6 +404,31 @@ int cad_scatter_cols_f32(const float* src, const int64_t* idx_dev, int64_t n,
 /* fp32 -> bf16 elementwise (dK/dV accumulators to output). */
 int cad_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 
+/* ---- copy-engine transport (CUDA IPC + stream memory operations) ------ */
+/* The export handle of the allocation holding `ptr` and ptr's offset in it. */
+int cad_ipc_handle(const void* ptr, uint8_t handle[64], int64_t* offset);
+/* Maps a peer allocation (cudaIpcOpenMemHandle, lazy peer access). */
+int cad_ipc_open(const uint8_t handle[64], void** base);
+int cad_ipc_close(void* base);
+
+/* A run of consecutive rows: rows [src_row, src_row+n_rows) -> [dst_row, ...). */
+typedef struct cad_run {
+  int64_t src_row;
+  int64_t dst_row;
+  int64_t n_rows;
+} cad_run;
+/* One cudaMemcpyAsync per run (copy engines; dst may be a peer mapping). */
+int cad_copy_runs(const cad_run* runs, int64_t n, const void* src, void* dst,
+                  int64_t row_bytes, void* stream);
+/* Runs of a [heads][rows] fp32 matrix (LSE): one 2-D copy per run. */
+int cad_copy_runs_cols(const cad_run* runs, int64_t n, const float* src,
+                       int64_t src_rows, float* dst, int64_t dst_rows,
+                       int32_t heads, void* stream);
+/* GPU-side flags: write a 32-bit value once prior stream work is done, and
+ * make a stream wait until a (local) flag is >= value. */
+int cad_stream_write_u32(void* addr, uint32_t value, void* stream);
+int cad_stream_wait_u32(const void* addr, uint32_t value, void* stream);
+
 /* All-to-allv over the communicator (grouped ncclSend/ncclRecv), byte
  * counts and displacements per peer, on `stream`. */
 int cad_alltoallv(cad_comm* comm, const void* send, const int64_t* send_bytes,

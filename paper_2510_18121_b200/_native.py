@@ -100,6 +100,10 @@ class cad_xfer(C.Structure):
                 ("n_recv", i64)]
 
 
+class cad_run(C.Structure):
+    _fields_ = [("src_row", i64), ("dst_row", i64), ("n_rows", i64)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 
@@ -144,6 +148,13 @@ SIGNATURES = {
     "cad_gather_cols_f32": (C.c_int, [vp, i64, i32, vp, i64, vp, vp]),
     "cad_scatter_cols_f32": (C.c_int, [vp, vp, i64, i32, vp, i64, vp]),
     "cad_f32_to_bf16": (C.c_int, [vp, i64, vp, vp]),
+    "cad_ipc_handle": (C.c_int, [vp, P(u8), P(i64)]),
+    "cad_ipc_open": (C.c_int, [P(u8), P(vp)]),
+    "cad_ipc_close": (C.c_int, [vp]),
+    "cad_copy_runs": (C.c_int, [vp, i64, vp, vp, i64, vp]),
+    "cad_copy_runs_cols": (C.c_int, [vp, i64, vp, i64, vp, i64, i32, vp]),
+    "cad_stream_write_u32": (C.c_int, [vp, C.c_uint32, vp]),
+    "cad_stream_wait_u32": (C.c_int, [vp, C.c_uint32, vp]),
     "cad_comm_unique_id": (C.c_int, [P(u8)]),
     "cad_comm_init": (C.c_int, [P(u8), i32, i32, P(vp)]),
     "cad_comm_destroy": (C.c_int, [vp]),

@@ -6,6 +6,8 @@
 // NCCL is bound at run time (dlopen of libnccl.so.2): inside a process that
 // already runs torch.distributed this resolves to the NCCL torch loaded, so
 // both communicators share one library.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -132,6 +134,52 @@ unsigned blocks_for(int64_t work) {
 
 }  // namespace
 
+namespace {
+
+PFN_cuStreamWriteValue32_v11070 write_value_fn() {
+  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 11070, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+  });
+  if (!fn) throw cad::CudaError("cuStreamWriteValue32 unavailable");
+  return fn;
+}
+
+PFN_cuStreamWaitValue32_v11070 wait_value_fn() {
+  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 11070, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  });
+  if (!fn) throw cad::CudaError("cuStreamWaitValue32 unavailable");
+  return fn;
+}
+
+PFN_cuMemGetAddressRange_v3020 addr_range_fn() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &p, 3020, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  if (!fn) throw cad::CudaError("cuMemGetAddressRange unavailable");
+  return fn;
+}
+
+}  // namespace
+
 struct cad_comm {
   ncclComm_t comm = nullptr;
   int32_t rank = 0, world = 1;
@@ -253,6 +301,85 @@ int cad_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream) {
     f32_to_bf16_kernel<<<blocks_for(n / 4), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<const float4*>(src), n / 4, static_cast<uint2*>(dst));
     cad_dev::cuda_check(cudaGetLastError(), "f32_to_bf16");
+  });
+}
+
+int cad_ipc_handle(const void* ptr, uint8_t handle[64], int64_t* offset) {
+  return cad::guarded([&] {
+    if (!ptr || !handle || !offset) throw cad::DomainError("null argument");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (addr_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+      throw cad::CudaError("cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    cad_dev::cuda_check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(handle, &h, 64);
+    *offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  });
+}
+
+int cad_ipc_open(const uint8_t handle[64], void** base) {
+  return cad::guarded([&] {
+    if (!handle || !base) throw cad::DomainError("null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    cad_dev::cuda_check(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int cad_ipc_close(void* base) {
+  return cad::guarded([&] {
+    if (base) cad_dev::cuda_check(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+  });
+}
+
+int cad_copy_runs(const cad_run* runs, int64_t n, const void* src, void* dst, int64_t row_bytes, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!runs || !src || !dst) throw cad::DomainError("null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int64_t i = 0; i < n; ++i) {
+      const cad_run& r = runs[i];
+      cad_dev::cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + r.dst_row * row_bytes,
+                                          static_cast<const char*>(src) + r.src_row * row_bytes,
+                                          static_cast<size_t>(r.n_rows * row_bytes), cudaMemcpyDeviceToDevice, s),
+                          "cudaMemcpyAsync(run)");
+    }
+  });
+}
+
+int cad_copy_runs_cols(const cad_run* runs, int64_t n, const float* src, int64_t src_rows, float* dst,
+                       int64_t dst_rows, int32_t heads, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!runs || !src || !dst) throw cad::DomainError("null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int64_t i = 0; i < n; ++i) {
+      const cad_run& r = runs[i];
+      cad_dev::cuda_check(cudaMemcpy2DAsync(dst + r.dst_row, static_cast<size_t>(dst_rows) * 4, src + r.src_row,
+                                            static_cast<size_t>(src_rows) * 4, static_cast<size_t>(r.n_rows) * 4,
+                                            static_cast<size_t>(heads), cudaMemcpyDeviceToDevice, s),
+                          "cudaMemcpy2DAsync(run)");
+    }
+  });
+}
+
+int cad_stream_write_u32(void* addr, uint32_t value, void* stream) {
+  return cad::guarded([&] {
+    if (!addr) throw cad::DomainError("null argument");
+    if (write_value_fn()(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                         CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      throw cad::CudaError("cuStreamWriteValue32 failed");
+  });
+}
+
+int cad_stream_wait_u32(const void* addr, uint32_t value, void* stream) {
+  return cad::guarded([&] {
+    if (!addr) throw cad::DomainError("null argument");
+    if (wait_value_fn()(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                        CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      throw cad::CudaError("cuStreamWaitValue32 failed");
   });
 }
 

@@ -188,6 +188,7 @@ class DistCALayer:
         self.send_buf = torch.empty(max_bytes, dtype=torch.uint8, device=device)
         self.recv_buf = torch.empty(max_bytes, dtype=torch.uint8, device=device)
         self.launches = 0
+        self.ce = None
 
     # ---------------------------------------------------------------- exchange
     def _exchange(self, dx: _DevXfer, src: torch.Tensor, dst: torch.Tensor, row_bytes: int, stream,
@@ -257,12 +258,23 @@ class DistCALayer:
             self.launches += 3
 
     # ---------------------------------------------------------------- step
+    def use_copy_engines(self, all_plans: List[LayerPlan], o, lse, dq):
+        """Switch the exchanges to the copy-engine transport (CUDA IPC pushes);
+        o/lse/dq become the registered home output buffers of every step."""
+        self.ce = CETransport(self, all_plans, o, lse, dq)
+
     def step(self, q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode: str = "pingpong"):
         """One layer fwd+bwd. mode: 'pingpong' (comm of one half under CA of
         the other), 'serial' (single stream, no overlap), 'compute' (CA
         kernels only; server buffers assumed resident: the reference's
         'signal' bound), 'comm' (exchanges only)."""
         comp = torch.cuda.current_stream(self.dev)
+        if mode in ("pingpong", "comm", "signal") and getattr(self, "ce", None) is not None:
+            if not (o.data_ptr() == self.ce.o.data_ptr() and dq.data_ptr() == self.ce.dq.data_ptr()
+                    and lse.data_ptr() == self.ce.lse.data_ptr()):
+                raise ValueError("copy-engine transport: outputs must be the registered home buffers")
+            self.ce.step(q, k, v, do, dk_acc, dv_acc, compute=(mode != "comm"), move=(mode != "signal"))
+            return
         comm = self.comm_stream if mode == "pingpong" else comp
         ev = lambda: torch.cuda.Event()
         dk_acc.zero_()
@@ -325,3 +337,215 @@ class DistCALayer:
         fin = ev()
         fin.record(comm)
         comp.wait_event(fin)
+
+
+# --------------------------------------------------------------------------
+# Copy-engine transport: every rank pushes its rows straight into the peers'
+# buffers (CUDA IPC mappings) with cudaMemcpyAsync, so no SM is taken from
+# the persistent CA kernels; GPU-side 32-bit flags (cuStreamWriteValue32 on
+# the peer's flag word after the copies, cuStreamWaitValue32 on the local
+# word before use) order producer and consumer streams across processes
+# without host synchronisation.
+
+F_QKV, F_DO, F_O, F_G, F_DONE = 0, 1, 2, 3, 4  # flag kinds (x2 halves, F_DONE uses half 0)
+
+
+def _runs(src: np.ndarray, dst: np.ndarray) -> np.ndarray:
+    """Maximal runs where both src and dst rows advance by one."""
+    if len(src) == 0:
+        return np.zeros((0, 3), dtype=np.int64)
+    brk = np.nonzero((np.diff(src) != 1) | (np.diff(dst) != 1))[0] + 1
+    starts = np.concatenate([[0], brk])
+    ends = np.concatenate([brk, [len(src)]])
+    return np.stack([src[starts], dst[starts], ends - starts], axis=1).astype(np.int64)
+
+
+def _split(counts, arr):
+    out, o = [], 0
+    for c in counts:
+        out.append(arr[o:o + int(c)])
+        o += int(c)
+    return out
+
+
+class _RunList:
+    def __init__(self, runs: np.ndarray):
+        self.n = len(runs)
+        self.arr = (N.cad_run * max(1, self.n))()
+        for i, (a, b, c) in enumerate(runs.tolist()):
+            self.arr[i] = N.cad_run(a, b, c)
+
+
+class CETransport:
+    """Row pushes over CUDA IPC for one DistCALayer. Needs every rank's
+    LayerPlan (all ranks build them deterministically)."""
+
+    def __init__(self, layer: "DistCALayer", all_plans: List[LayerPlan], o, lse, dq):
+        import torch.distributed as dist
+        self.layer, self.plans = layer, all_plans
+        lp = layer.lp
+        W, me = lp.world, lp.rank
+        self.W, self.me = W, me
+        dev = layer.dev
+        self.o, self.lse, self.dq = o, lse, dq
+        # dK/dV partial staging per half (rows in this rank's KV_RET recv order)
+        self.stage = []
+        for hp in lp.halves:
+            n = max(1, hp.xfers[XFER_KV_RET].n_recv)
+            self.stage.append({"dk": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
+                               "dv": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
+                               "idx": layer.halves[lp.halves.index(hp)]["x"][XFER_KV_RET].recv_idx})
+        self.flags = torch.zeros(16 * W, dtype=torch.int32, device=dev)
+        # buffers peers write into, exported once
+        local = {"flags": self.flags, "o": o, "lse": lse, "dq": dq}
+        for h, H in enumerate(layer.halves):
+            for n_ in ("q", "k", "v", "do"):
+                local[f"{n_}{h}"] = H[n_]
+            local[f"sdk{h}"] = self.stage[h]["dk"]
+            local[f"sdv{h}"] = self.stage[h]["dv"]
+        mine = {}
+        for name, t in local.items():
+            hb = (N.u8 * 64)()
+            off = N.i64()
+            check(lib().cad_ipc_handle(t.data_ptr(), hb, C.byref(off)))
+            mine[name] = (bytes(hb), off.value)
+        allh = [None] * W
+        dist.all_gather_object(allh, mine)
+        self.bases = []  # opened peer bases (to close)
+        self.peer = []   # peer -> name -> device pointer
+        for p in range(W):
+            if p == me:
+                self.peer.append({k: t.data_ptr() for k, t in local.items()})
+                continue
+            opened, ptrs = {}, {}
+            for name, (hb, off) in allh[p].items():
+                if hb not in opened:
+                    base = C.c_void_p()
+                    check(lib().cad_ipc_open((N.u8 * 64).from_buffer_copy(hb), C.byref(base)))
+                    opened[hb] = base.value
+                    self.bases.append(base.value)
+                ptrs[name] = opened[hb] + off
+            self.peer.append(ptrs)
+        # row runs per (half, exchange, peer): what this rank pushes
+        self.runs = {}
+        for h in (0, 1):
+            for x in range(4):
+                mine_x = lp.halves[h].xfers[x]
+                sends = _split(mine_x.send_counts, mine_x.send_idx)
+                for p in range(W):
+                    px = all_plans[p].halves[h].xfers[x]
+                    dst = _split(px.recv_counts, px.recv_idx)[me]
+                    if x == XFER_KV_RET:  # partials land in the owner's staging, in recv order
+                        disp = int(px.recv_counts[:me].sum())
+                        dst = np.arange(disp, disp + len(dst), dtype=np.int64)
+                    self.runs[(h, x, p)] = _RunList(_runs(sends[p], dst))
+        self.gen = 0
+        self.launches = 0
+        self.move = True
+
+    def close(self):
+        for b in self.bases:
+            lib().cad_ipc_close(b)
+        self.bases = []
+
+    # flag word of (kind, half, src) on rank p
+    def _flag(self, p, kind, h, src):
+        return self.peer[p]["flags"] + 4 * ((kind * 2 + h) * self.W + src)
+
+    def _signal(self, kind, h, stream):
+        for p in range(self.W):
+            check(lib().cad_stream_write_u32(self._flag(p, kind, h, self.me), self.gen, stream.cuda_stream))
+
+    def _await(self, kind, h, stream, value=None):
+        v = self.gen if value is None else value
+        for src in range(self.W):
+            check(lib().cad_stream_wait_u32(self._flag(self.me, kind, h, src), v, stream.cuda_stream))
+
+    def _push(self, h, x, src, dst_name, row_bytes, stream):
+        if not self.move:
+            return
+        for p in range(self.W):
+            rl = self.runs[(h, x, p)]
+            if rl.n:
+                check(lib().cad_copy_runs(rl.arr, rl.n, src.data_ptr(), self.peer[p][dst_name], row_bytes,
+                                          stream.cuda_stream))
+
+    def _push_lse(self, h, src_lse, stream):
+        if not self.move:
+            return
+        L = self.layer
+        for p in range(self.W):
+            rl = self.runs[(h, XFER_O_RET, p)]
+            if rl.n:
+                dst_rows = self.plans[p].home_rows
+                check(lib().cad_copy_runs_cols(rl.arr, rl.n, src_lse.data_ptr(), src_lse.shape[1],
+                                               self.peer[p]["lse"], dst_rows, L.hq, stream.cuda_stream))
+
+    def step(self, q, k, v, do, dk_acc, dv_acc, compute: bool = True, move: bool = True):
+        """One layer. compute=False moves the same rows without running the
+        CA kernels (comm-only time); move=False keeps every flag/ordering but
+        skips the row copies (the reference's 'signal' mode, sim.hpp:14-18,
+        where each transfer shrinks to a message)."""
+        L = self.layer
+        self.move = move
+        comp = torch.cuda.current_stream(L.dev)
+        comm = L.comm_stream
+        self.gen += 1
+        g = self.gen
+        start = torch.cuda.Event()
+        start.record(comp)
+        comm.wait_event(start)
+        # every peer finished step g-1 (its buffers are free to overwrite)
+        self._await(F_DONE, 0, comm, g - 1)
+        # host enqueue order interleaves the two streams so the first CA
+        # kernel is queued as soon as its inputs are, not after every push
+        fwd_done, bwd_done = [], []
+
+        def dispatch_qkv(h):
+            self._push(h, XFER_Q, q, f"q{h}", L.q_row, comm)
+            self._push(h, XFER_KV, k, f"k{h}", L.kv_row, comm)
+            self._push(h, XFER_KV, v, f"v{h}", L.kv_row, comm)
+            self._signal(F_QKV, h, comm)
+
+        def ca(h, fwd):
+            self._await(F_QKV if fwd else F_DO, h, comp)
+            if compute:
+                (L.ca_fwd if fwd else L.ca_bwd)(h, comp)
+            e = torch.cuda.Event()
+            e.record(comp)
+            (fwd_done if fwd else bwd_done).append(e)
+
+        dispatch_qkv(0)
+        ca(0, True)
+        dispatch_qkv(1)
+        for h in (0, 1):
+            self._push(h, XFER_Q, do, f"do{h}", L.q_row, comm)
+            self._signal(F_DO, h, comm)
+        ca(1, True)
+        for h in (0, 1):
+            comm.wait_event(fwd_done[h])
+            H = L.halves[h]
+            self._push(h, XFER_O_RET, H["o"], "o", L.q_row, comm)
+            self._push_lse(h, H["lse"], comm)
+            self._signal(F_O, h, comm)
+            ca(h, False)
+        for h in (0, 1):
+            comm.wait_event(bwd_done[h])
+            H = L.halves[h]
+            self._push(h, XFER_O_RET, H["dq"], "dq", L.q_row, comm)
+            self._push(h, XFER_KV_RET, H["dk"], f"sdk{h}", L.kv_row, comm)
+            self._push(h, XFER_KV_RET, H["dv"], f"sdv{h}", L.kv_row, comm)
+            self._signal(F_G, h, comm)
+        dk_acc.zero_()
+        dv_acc.zero_()
+        for h in (0, 1):
+            self._await(F_O, h, comp)
+            self._await(F_G, h, comp)
+            st = self.stage[h]
+            n = L.lp.halves[h].xfers[XFER_KV_RET].n_recv
+            check(lib().cad_scatter_add_bf16(st["dk"].data_ptr(), st["idx"].data_ptr(), n, L.hkv * L.d,
+                                             dk_acc.data_ptr(), comp.cuda_stream))
+            check(lib().cad_scatter_add_bf16(st["dv"].data_ptr(), st["idx"].data_ptr(), n, L.hkv * L.d,
+                                             dv_acc.data_ptr(), comp.cuda_stream))
+            self.launches += 2
+        self._signal(F_DONE, 0, comp)

@@ -45,7 +45,12 @@ def main():
     dq = torch.empty_like(home["q"])
     dk_acc = torch.zeros(H, shape.h_kv, 128, device=dev)
     dv_acc = torch.zeros_like(dk_acc)
-    for mode in ("pingpong", "serial"):
+    transport = os.environ.get("CAD_TRANSPORT", "ce")
+    if transport == "ce":
+        plans = [D.LayerPlan(lengths, world, r, shape) for r in range(world)]
+        layer.use_copy_engines(plans, o, lse, dq)
+    for mode in ("pingpong", "serial", "pingpong"):
+        o.zero_(); dq.zero_(); lse.zero_()
         layer.step(home["q"], home["k"], home["v"], home["do"], o, lse, dq, dk_acc, dv_acc, mode=mode)
     torch.cuda.synchronize()
     # whole batch on this GPU
@@ -62,7 +67,7 @@ def main():
         "dq": (dq.float() - rdq[rows_d].float()).abs().max().item(),
         "dk": (dk_acc - rdk[rows_d].float()).abs().max().item(),
         "dv": (dv_acc - rdv[rows_d].float()).abs().max().item(),
-        "migrations": lp.plan.migrations, "rank": rank,
+        "migrations": lp.plan.migrations, "rank": rank, "transport": transport,
     }
     scale = {"dq": rdq.float().abs().max().item(), "dk": rdk.float().abs().max().item(),
              "dv": rdv.float().abs().max().item()}
