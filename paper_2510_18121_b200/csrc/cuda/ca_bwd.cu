@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           if (++st == kStages) { st = 0; ph ^= 1; }
         }
       }
-    } else if (warp == 9 && lane == 0) {
+    } else if (warp == 9) {
       // ---------------------------------------------------------- MMA
       uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0;
       uint32_t p_ph[2] = {0, 0}, ds_ph[2] = {0, 0};
@@ -296,9 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           mbar_wait(&bars->in_full[s], par);
           tc_fence_after();
           issue_qk_n<kSub>(tmem + 128 * i, sK, sbase + kQOff + s * kSubBytes);
-          umma_commit(&bars->s_full[i]);
+          mma_commit(&bars->s_full[i]);
           issue_qk_n<kSub>(tmem + 128 * i + 64, sV, sbase + kDOOff + s * kSubBytes);
-          umma_commit(&bars->dp_full[i]);
+          mma_commit(&bars->dp_full[i]);
         }
         for (int i = 0; i < n; ++i) {
           const int b = i & 1;
@@ -322,20 +322,20 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
             mbar_wait(&bars->in_full[s2], par2);
             tc_fence_after();
             issue_qk_n<kSub>(tSb, sK, sbase + kQOff + s2 * kSubBytes);
-            umma_commit(&bars->s_full[b]);
+            mma_commit(&bars->s_full[b]);
           }
           mbar_wait(&bars->ds_full[b], ds_ph[b]);
           ds_ph[b] ^= 1;
           tc_fence_after();
           issue_pv_k<kSub>(tDK, tDPb, sbase + kQOff + s * kSubBytes, i > 0);  // dK += dS^T Q
-          umma_commit(&bars->in_empty[s]);
+          mma_commit(&bars->in_empty[s]);
           if (more) {
             issue_qk_n<kSub>(tDPb, sV, sbase + kDOOff + s2 * kSubBytes);
-            umma_commit(&bars->dp_full[b]);
+            mma_commit(&bars->dp_full[b]);
           }
         }
-        umma_commit(&bars->acc_full);
-        umma_commit(&bars->kv_empty);
+        mma_commit(&bars->acc_full);
+        mma_commit(&bars->kv_empty);
         const uint32_t lin = st + n;
         st = lin % kStages;
         ph ^= (lin / kStages) & 1;
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           if (++st == 2) { st = 0; ph ^= 1; }
         }
       }
-    } else if (warp == 9 && lane == 0) {
+    } else if (warp == 9) {
       uint32_t q_it = 0, st = 0, ph = 0, dq_it = 0, pr_ph = 0, ds_ph = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const FwdUnit un = p.units[u];
@@ -542,9 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         tc_fence_after();
         const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
         issue_qk(tS, sQ, sbase + kKOff + st * kTileBytes);
-        umma_commit(&bars->s_full);
+        mma_commit(&bars->s_full);
         issue_qk(tDP, sDO, sbase + kVOff + st * kTileBytes);
-        umma_commit(&bars->dp_full);
+        mma_commit(&bars->dp_full);
         for (int j = 0; j < n; ++j) {
           const uint32_t cur = st;
           uint32_t nst = st, nph = ph;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
             mbar_wait(&bars->kv_full[nst], nph);
             tc_fence_after();
             issue_qk(tS, sQ, sbase + kKOff + nst * kTileBytes);  // S(j+1)
-            umma_commit(&bars->s_full);
+            mma_commit(&bars->s_full);
           } else {
             mbar_wait(&bars->p_read, pr_ph);
             pr_ph ^= 1;
@@ -569,16 +569,16 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           tc_fence_after();
           const uint32_t ds = tDS + (j & 1) * 64;
           issue_pv(tDQ, ds, ds + 32, sbase + kKOff + cur * kTileBytes, j > 0);  // dQ += dS K
-          umma_commit(&bars->kv_empty[cur]);
+          mma_commit(&bars->kv_empty[cur]);
           if (j + 1 < n) {
             issue_qk(tDP, sDO, sbase + kVOff + nst * kTileBytes);  // dP(j+1)
-            umma_commit(&bars->dp_full);
+            mma_commit(&bars->dp_full);
           }
           st = nst;
           ph = nph;
         }
-        umma_commit(&bars->dq_full);
-        umma_commit(&bars->q_empty);
+        mma_commit(&bars->dq_full);
+        mma_commit(&bars->q_empty);
         if (++st == 2) { st = 0; ph ^= 1; }
       }
     }

@@ -142,60 +142,58 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
-      uint32_t pph[2] = {0, 0}, fph[2] = {0, 0};
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const FwdUnit un = p.units[u];
-        const int n = un.n_kv, nh = un.nh;
-        dbg_mark(1, 0x100);
-        mbar_wait(&bars->q_full, q_it & 1);
-        ++q_it;
-        dbg_mark(1, 0x200);
-        mbar_wait(&bars->k_full[ks], kph);
+    uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
+    uint32_t pph[2] = {0, 0}, fph[2] = {0, 0};
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const FwdUnit un = p.units[u];
+      const int n = un.n_kv, nh = un.nh;
+      dbg_mark(1, 0x100);
+      mbar_wait(&bars->q_full, q_it & 1);
+      ++q_it;
+      dbg_mark(1, 0x200);
+      mbar_wait(&bars->k_full[ks], kph);
+      tc_fence_after();
+      for (int h = 0; h < nh; ++h) {
+        issue_qk(tmem + h * 128, sbase + kQOff + h * kTileBytes, sbase + kKOff + ks * kTileBytes);
+        mma_commit(&bars->s_full[h]);
+      }
+      mma_commit(&bars->k_empty[ks]);
+      if (++ks == 2) { ks = 0; kph ^= 1; }
+      if (n == 1) mma_commit(&bars->q_empty);
+      for (int j = 0; j < n; ++j) {
+        dbg_mark(1, 0x300 + j);
+        mbar_wait(&bars->v_full[vs], vph);
         tc_fence_after();
         for (int h = 0; h < nh; ++h) {
-          issue_qk(tmem + h * 128, sbase + kQOff + h * kTileBytes, sbase + kKOff + ks * kTileBytes);
-          umma_commit(&bars->s_full[h]);
-        }
-        umma_commit(&bars->k_empty[ks]);
-        if (++ks == 2) { ks = 0; kph ^= 1; }
-        if (n == 1) umma_commit(&bars->q_empty);
-        for (int j = 0; j < n; ++j) {
-          dbg_mark(1, 0x300 + j);
-          mbar_wait(&bars->v_full[vs], vph);
+          dbg_mark(1, 0x400 + j * 16 + h);
+          mbar_wait(&bars->p_full[h], pph[h]);
+          dbg_mark(1, 0x500 + j * 16 + h);
+          pph[h] ^= 1;
+          if (j == 0) {
+            mbar_wait(&bars->o_free[h], fph[h] ^ 1);
+            fph[h] ^= 1;
+          }
           tc_fence_after();
-          for (int h = 0; h < nh; ++h) {
-            dbg_mark(1, 0x400 + j * 16 + h);
-            mbar_wait(&bars->p_full[h], pph[h]);
-            dbg_mark(1, 0x500 + j * 16 + h);
-            pph[h] ^= 1;
-            if (j == 0) {
-              mbar_wait(&bars->o_free[h], fph[h] ^ 1);
-              fph[h] ^= 1;
+          issue_pv(tmem + 256 + h * 128, tmem + h * 128, tmem + h * 128 + 32,
+                   sbase + kVOff + vs * kTileBytes, j > 0);
+          if (j == n - 1) {
+            mma_commit(&bars->o_full[h]);
+          } else {
+            if (h == 0) {
+              dbg_mark(1, 0x600 + j);
+              mbar_wait(&bars->k_full[ks], kph);
+              tc_fence_after();
             }
-            tc_fence_after();
-            issue_pv(tmem + 256 + h * 128, tmem + h * 128, tmem + h * 128 + 32,
-                     sbase + kVOff + vs * kTileBytes, j > 0);
-            if (j == n - 1) {
-              umma_commit(&bars->o_full[h]);
-            } else {
-              if (h == 0) {
-                dbg_mark(1, 0x600 + j);
-                mbar_wait(&bars->k_full[ks], kph);
-                tc_fence_after();
-              }
-              issue_qk(tmem + h * 128, sbase + kQOff + h * kTileBytes, sbase + kKOff + ks * kTileBytes);
-              umma_commit(&bars->s_full[h]);
-            }
+            issue_qk(tmem + h * 128, sbase + kQOff + h * kTileBytes, sbase + kKOff + ks * kTileBytes);
+            mma_commit(&bars->s_full[h]);
           }
-          umma_commit(&bars->v_empty[vs]);
-          if (++vs == 2) { vs = 0; vph ^= 1; }
-          if (j < n - 1) {
-            umma_commit(&bars->k_empty[ks]);
-            if (++ks == 2) { ks = 0; kph ^= 1; }
-            if (j + 1 == n - 1) umma_commit(&bars->q_empty);
-          }
+        }
+        mma_commit(&bars->v_empty[vs]);
+        if (++vs == 2) { vs = 0; vph ^= 1; }
+        if (j < n - 1) {
+          mma_commit(&bars->k_empty[ks]);
+          if (++ks == 2) { ks = 0; kph ^= 1; }
+          if (j + 1 == n - 1) mma_commit(&bars->q_empty);
         }
       }
     }

@@ -14,9 +14,16 @@
 
 namespace cad_dev {
 
+// The issue helpers are called by the whole (converged) MMA warp, so the
+// descriptors stay warp-uniform (uniform registers); one elect.sync-chosen
+// lane issues the tcgen05 ops and the commits. (Issuing from a lane-0-only
+// branch makes ptxas wrap every UTCHMMA in an R2UR/ELECT waterfall loop:
+// ~100 cycles per MMA, which throttled the tensor pipe.)
+
 // D = A B^T: M=128, N=128, K=128 (d) as 8 steps of 16.
 __device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint32_t a_smem, uint32_t b_smem) {
   constexpr uint32_t idesc = idesc_bf16(128, 128, false, false);
+  if (!elect_one()) return;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t off = (k >> 2) * (kTileBytes / 2) + (k & 3) * 32;
@@ -33,6 +40,7 @@ __device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint32_t a_smem, uint3
 __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
                                          uint32_t b_smem, bool accumulate) {
   constexpr uint32_t idesc = idesc_bf16(128, 128, false, true);
+  if (!elect_one()) return;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t a = k < 4 ? a_lo + k * 8 : a_hi + (k - 4) * 8;
@@ -47,6 +55,7 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t a_lo, uint32_
 template <int N>
 __device__ __forceinline__ void issue_qk_n(uint32_t d_tmem, uint32_t a_smem, uint32_t b_smem) {
   constexpr uint32_t idesc = idesc_bf16(128, N, false, false);
+  if (!elect_one()) return;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t kin = (k & 3) * 32;
@@ -61,11 +70,18 @@ template <int KR>
 __device__ __forceinline__ void issue_pv_k(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem,
                                            bool accumulate) {
   constexpr uint32_t idesc = idesc_bf16(128, 128, false, true);
+  if (!elect_one()) return;
 #pragma unroll
   for (int k = 0; k < KR / 16; ++k) {
     umma_ts(d_tmem, a_tmem + k * 8, sw128_desc(b_smem + k * 2048, KR * 128, 1024), idesc,
             (accumulate || k > 0) ? 1u : 0u);
   }
+}
+
+// Warp-level commit by the elected (issuing) lane.
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  if (elect_one()) umma_commit(bar);
+  __syncwarp();
 }
 
 }  // namespace cad_dev
