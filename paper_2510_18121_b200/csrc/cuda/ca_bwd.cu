@@ -131,26 +131,34 @@ __global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bf
 //   P^T / dS^T (bf16) overwrite the first 32 columns of S^T / dP^T.
 namespace kv {
 
-constexpr int kStages = 4;
-constexpr uint32_t kSubBytes = kSub * kHeadDim * 2;  // 16 KB
+// 128-row q tiles; all four GEMMs are M=128, N=128 (the tensor core reads
+// its SS operands from shared memory at a fixed rate, so N=64 MMAs ran
+// smem-bound).
+//   TMEM: S^T [0,128)  dP^T [128,256)  dV [256,384)  dK [384,512)
+//   P^T (bf16) overwrites S^T columns: warpgroup w's 64 q columns land in
+//   [64w, 64w+32); dS^T likewise in dP^T.
+// Iteration i: S^T(i), dP^T(i) -> both warpgroups (64 q columns each):
+// P^T -> p_full; dS^T -> ds_full. MMA order: dV(i) | S^T(i+1) | dK(i) |
+// dP^T(i+1), so the tensor core runs dV(i)+S^T(i+1) while the warpgroups
+// compute dS^T(i), and dK(i)+dP^T(i+1) while they exponentiate i+1.
+constexpr int kStages = 2;
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
-constexpr uint32_t kQOff = 2 * kTileBytes;                  // kStages x 16 KB
-constexpr uint32_t kDOOff = kQOff + kStages * kSubBytes;    // kStages x 16 KB
-constexpr uint32_t kRowOff = kDOOff + kStages * kSubBytes;  // [stage][LSE 64 | D 64] fp32
-constexpr uint32_t kBarOff = kRowOff + kStages * 512;
+constexpr uint32_t kQOff = 2 * kTileBytes;                  // kStages x 32 KB
+constexpr uint32_t kDOOff = kQOff + kStages * kTileBytes;   // kStages x 32 KB
+constexpr uint32_t kRowOff = kDOOff + kStages * kTileBytes; // [stage][-LSE 128 | -D 128] fp32
+constexpr uint32_t kBarOff = kRowOff + kStages * 1024;
 constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 
 struct Bars {
   uint64_t kv_full, kv_empty;
   uint64_t in_full[kStages], in_empty[kStages];
-  uint64_t s_full[2], dp_full[2], p_full[2], ds_full[2];
-  uint64_t acc_full, acc_free;
+  uint64_t s_full, dp_full, p_full, ds_full, acc_full, acc_free;
   uint32_t tmem_base;
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_k, tm_v, tm_do;  // q/do maps have 64-row boxes
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;
   const float* nlse2;   // -LSE * log2(e), [h_q][pitch]
   const float* ndelta;  // -D, [h_q][pitch]
   int64_t pitch;
@@ -166,23 +174,22 @@ struct Params {
   float scale_log2;  // softmax scale * log2(e)
 };
 
-// Iteration cursor over (head in group, segment, q sub-tile) of one unit.
+// Iteration cursor over (segment, q tile, head in group) of one unit. q tiles
+// are walked from the LAST one down to the first that sees the kv tile, so
+// co-running CTAs (consecutive kv tiles of one document) stream the same Q/dO
+// rows at the same time; the GQA heads are innermost.
 struct Cursor {
   int g, seg, qt;
   __device__ void start(const KvUnit& u, const KvSeg* segs) {
     g = 0;
     seg = u.seg_begin;
-    qt = segs[seg].qt_lo;
+    qt = segs[seg].qt_hi - 1;
   }
-  __device__ void next(const KvUnit& u, const KvSeg* segs) {
-    if (++qt < segs[seg].qt_hi) return;
-    if (++seg < u.seg_end) {
-      qt = segs[seg].qt_lo;
-      return;
-    }
-    ++g;
-    seg = u.seg_begin;
-    qt = segs[seg].qt_lo;
+  __device__ void next(const KvUnit& u, const KvSeg* segs, int group) {
+    if (++g < group) return;
+    g = 0;
+    if (--qt >= segs[seg].qt_lo) return;
+    if (++seg < u.seg_end) qt = segs[seg].qt_hi - 1;
   }
 };
 
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
-  float* rows = reinterpret_cast<float*>(smem + kRowOff);  // [stage][lse 64 | d 64]
+  float* rows = reinterpret_cast<float*>(smem + kRowOff);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t warp = warp_id(), lane = lane_id();
 
@@ -205,12 +212,10 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       mbar_init(&bars->in_full[i], 33);
       mbar_init(&bars->in_empty[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars->s_full[b], 1);
-      mbar_init(&bars->dp_full[b], 1);
-      mbar_init(&bars->p_full[b], 128);
-      mbar_init(&bars->ds_full[b], 128);
-    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_full, 256);
+    mbar_init(&bars->ds_full, 256);
     mbar_init(&bars->acc_full, 1);
     mbar_init(&bars->acc_free, 256);
     fence_barrier_init();
@@ -220,16 +225,16 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  const uint32_t tDV = tmem + 256, tDK = tmem + 384;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
 
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 8) {
       // ---------------------------------------------------------- producer
-      // Lane 0 issues the TMA tile loads; the whole warp copies the
-      // sub-tile's 64 -LSE and 64 -D values (arbitrary, unaligned row offsets,
-      // so cp.async rather than TMA) and each lane's async arrive lands on
-      // in_full when its copies have (count 1 + 32).
+      // Lane 0 issues the TMA tile loads; the whole warp copies the tile's
+      // 128 -LSE and 128 -D values (arbitrary, unaligned row offsets, so
+      // cp.async rather than TMA); each lane's async arrive lands on in_full
+      // when its copies have (count 1 + 32).
       uint32_t kv_it = 0, st = 0, ph = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const KvUnit un = p.units[u];
@@ -245,30 +250,30 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         ++kv_it;
         Cursor c;
         c.start(un, p.segs);
-        for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
+        for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs, p.group)) {
           const DevTask tk = p.tasks[p.segs[c.seg].task];
           const int head = un.hk * p.group + c.g;
-          const int qrow = tk.q_off + c.qt * kSub;
+          const int qrow = tk.q_off + c.qt * kTile;
           mbar_wait(&bars->in_empty[st], ph ^ 1);
           if (lane == 0) {
-            mbar_expect_tx(&bars->in_full[st], 2 * kSubBytes);
-            uint8_t* q = smem + kQOff + st * kSubBytes;
-            uint8_t* d = smem + kDOOff + st * kSubBytes;
+            mbar_expect_tx(&bars->in_full[st], 2 * kTileBytes);
+            uint8_t* q = smem + kQOff + st * kTileBytes;
+            uint8_t* d = smem + kDOOff + st * kTileBytes;
             tma_load_3d(&p.tm_q, &bars->in_full[st], q, 0, qrow, head);
-            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kSubBytes / 2, 64, qrow, head);
+            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kTileBytes / 2, 64, qrow, head);
             tma_load_3d(&p.tm_do, &bars->in_full[st], d, 0, qrow, head);
-            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kSubBytes / 2, 64, qrow, head);
+            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kTileBytes / 2, 64, qrow, head);
           }
-          float* dst = rows + st * 128;
+          float* dst = rows + st * 256;
           const float* nl = p.nlse2 + int64_t(head) * p.pitch;
           const float* nd = p.ndelta + int64_t(head) * p.pitch;
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
+          for (int k = 0; k < 4; ++k) {
             const int col = lane + 32 * k;
             // rows past the buffer only feed masked columns: clamp the source
             const int64_t rrow = min(int64_t(qrow) + col, p.pitch - 1);
             cp_async4(dst + col, nl + rrow);
-            cp_async4(dst + 64 + col, nd + rrow);
+            cp_async4(dst + 128 + col, nd + rrow);
           }
           cp_async_arrive(&bars->in_full[st]);
           if (++st == kStages) { st = 0; ph ^= 1; }
@@ -276,104 +281,89 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       }
     } else if (warp == 9) {
       // ---------------------------------------------------------- MMA
-      uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0;
-      uint32_t p_ph[2] = {0, 0}, ds_ph[2] = {0, 0};
+      uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0, p_ph = 0, ds_ph = 0;
       const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const KvUnit un = p.units[u];
         const int n = un.n_iter;
         mbar_wait(&bars->kv_full, kv_it & 1);
         ++kv_it;
-        // stage of iteration i is (st + i) % kStages with parity flips at wrap
-        auto stage_of = [&](int i, uint32_t& s, uint32_t& par) {
-          const uint32_t lin = st + i;
-          s = lin % kStages;
-          par = ph ^ ((lin / kStages) & 1);
-        };
-        for (int i = 0; i < 2 && i < n; ++i) {
-          uint32_t s, par;
-          stage_of(i, s, par);
-          mbar_wait(&bars->in_full[s], par);
-          tc_fence_after();
-          issue_qk_n<kSub>(tmem + 128 * i, sK, sbase + kQOff + s * kSubBytes);
-          mma_commit(&bars->s_full[i]);
-          issue_qk_n<kSub>(tmem + 128 * i + 64, sV, sbase + kDOOff + s * kSubBytes);
-          mma_commit(&bars->dp_full[i]);
-        }
+        mbar_wait(&bars->in_full[st], ph);
+        tc_fence_after();
+        uint32_t sQ = sbase + kQOff + st * kTileBytes, sDO = sbase + kDOOff + st * kTileBytes;
+        issue_qk(tS, sK, sQ);
+        mma_commit(&bars->s_full);
+        issue_qk(tDP, sV, sDO);
+        mma_commit(&bars->dp_full);
         for (int i = 0; i < n; ++i) {
-          const int b = i & 1;
-          uint32_t s, par;
-          stage_of(i, s, par);
-          const uint32_t tSb = tmem + 128 * b, tDPb = tSb + 64;
-          mbar_wait(&bars->p_full[b], p_ph[b]);
-          p_ph[b] ^= 1;
+          const uint32_t cur = st;
+          mbar_wait(&bars->p_full, p_ph);
+          p_ph ^= 1;
           if (i == 0) {
             mbar_wait(&bars->acc_free, (acc_it & 1) ^ 1);
             ++acc_it;
           }
           tc_fence_after();
-          issue_pv_k<kSub>(tDV, tSb, sbase + kDOOff + s * kSubBytes, i > 0);  // dV += P^T dO
-          // S^T(i+2) may overwrite buffer b as soon as dV(i) (which reads P^T
-          // there) is issued: tcgen05 MMAs execute in issue order.
-          uint32_t s2 = 0, par2 = 0;
-          const bool more = i + 2 < n;
-          if (more) {
-            stage_of(i + 2, s2, par2);
-            mbar_wait(&bars->in_full[s2], par2);
+          issue_pv(tDV, tS, tS + 64, sDO, i > 0);  // dV += P^T dO
+          uint32_t nQ = 0, nDO = 0;
+          if (i + 1 < n) {
+            if (++st == kStages) { st = 0; ph ^= 1; }
+            mbar_wait(&bars->in_full[st], ph);
             tc_fence_after();
-            issue_qk_n<kSub>(tSb, sK, sbase + kQOff + s2 * kSubBytes);
-            mma_commit(&bars->s_full[b]);
+            nQ = sbase + kQOff + st * kTileBytes;
+            nDO = sbase + kDOOff + st * kTileBytes;
+            issue_qk(tS, sK, nQ);  // S^T(i+1): runs after dV(i) read P^T (in order)
+            mma_commit(&bars->s_full);
           }
-          mbar_wait(&bars->ds_full[b], ds_ph[b]);
-          ds_ph[b] ^= 1;
+          mbar_wait(&bars->ds_full, ds_ph);
+          ds_ph ^= 1;
           tc_fence_after();
-          issue_pv_k<kSub>(tDK, tDPb, sbase + kQOff + s * kSubBytes, i > 0);  // dK += dS^T Q
-          mma_commit(&bars->in_empty[s]);
-          if (more) {
-            issue_qk_n<kSub>(tDPb, sV, sbase + kDOOff + s2 * kSubBytes);
-            mma_commit(&bars->dp_full[b]);
+          issue_pv(tDK, tDP, tDP + 64, sQ, i > 0);  // dK += dS^T Q
+          mma_commit(&bars->in_empty[cur]);
+          if (i + 1 < n) {
+            issue_qk(tDP, sV, nDO);  // dP^T(i+1)
+            mma_commit(&bars->dp_full);
+            sQ = nQ;
+            sDO = nDO;
           }
         }
         mma_commit(&bars->acc_full);
         mma_commit(&bars->kv_empty);
-        const uint32_t lin = st + n;
-        st = lin % kStages;
-        ph ^= (lin / kStages) & 1;
+        if (++st == kStages) { st = 0; ph ^= 1; }
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------------------ elementwise
-    const int wg = warp >> 2;                   // handles iterations i with i % 2 == wg
+    const int w = warp >> 2;                    // q columns [64w, 64w+64)
     const uint32_t r = (warp & 3) * 32 + lane;  // kv row within the tile
     const uint32_t lsel = ((warp & 3) * 32) << 16;
-    const uint32_t tSb = tmem + lsel + 128 * wg, tDPb = tSb + 64;
+    const int c0 = 64 * w;
+    const uint32_t tSw = tS + lsel, tDPw = tDP + lsel;
     uint32_t st = 0, ph = 0, s_ph = 0, dp_ph = 0, acc_ph = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const KvUnit un = p.units[u];
       const int kj = un.tile * kTile + r;  // key index relative to kv_off
       Cursor c;
       c.start(un, p.segs);
-      for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs)) {
-        const uint32_t cur = st, cur_ph = ph;
-        if (++st == kStages) { st = 0; ph ^= 1; }
-        if ((i & 1) != wg) continue;
+      for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs, p.group)) {
         const DevTask tk = p.tasks[p.segs[c.seg].task];
         const int shift = tk.kv_len - tk.n_q;
-        const int q0 = c.qt * kSub;  // query index of column 0
-        mbar_wait_warp(&bars->in_full[cur], cur_ph);
-        const uint32_t s_nlse = smem_u32(rows + cur * 128), s_nd = s_nlse + 256;
-        mbar_wait_warp(&bars->s_full[wg], s_ph);
+        const int q0 = c.qt * kTile + c0;  // query index of this thread's column 0
+        mbar_wait_warp(&bars->in_full[st], ph);
+        const uint32_t s_nlse = smem_u32(rows + st * 256 + c0), s_nd = s_nlse + 512;
+        if (++st == kStages) { st = 0; ph ^= 1; }
+        mbar_wait_warp(&bars->s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
         float x[64];
-        load_row64(tSb, x);
-        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q; the
-        // sub-tile is mask-free (CTA-uniform) when the last kv row of the tile
-        // is visible from column 0 and all 64 columns are real queries.
+        load_row64(tSw + c0, x);
+        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q; this
+        // warpgroup's 64 columns are mask-free (CTA-uniform) when the tile's
+        // last kv row is visible from column 0 and all columns are queries.
         const int lo = kj - shift - q0;
         const int hi = tk.n_q - q0;
-        const bool full = (un.tile * kTile + kTile - 1 - shift - q0) <= 0 && hi >= kSub;
+        const bool full = (un.tile * kTile + kTile - 1 - shift - q0) <= 0 && hi >= 64;
         const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
 #pragma unroll
         for (int k = 0; k < 64; k += 4) {
@@ -390,15 +380,15 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
 #pragma unroll
           for (int k = 0; k < 64; ++k) x[k] = (k >= lo && k < hi) ? x[k] : 0.f;
         }
-        store_bf16_64(tSb, x);  // P^T into the first 32 columns of S^T
+        store_bf16_64(tSw + 64 * w, x);  // P^T: WG0 -> cols [0,32), WG1 -> [64,96)
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->p_full[wg]);
-        mbar_wait_warp(&bars->dp_full[wg], dp_ph);
+        mbar_arrive(&bars->p_full);
+        mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
         float y[64];
-        load_row64(tDPb, y);
+        load_row64(tDPw + c0, y);
 #pragma unroll
         for (int k = 0; k < 64; k += 4) {
           const float4 nd = lds4(s_nd + 4 * k);
@@ -410,16 +400,15 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
 #pragma unroll
           for (int k = 0; k < 64; ++k) y[k] = (k >= lo && k < hi) ? y[k] : 0.f;
         }
-        store_bf16_64(tDPb, y);  // dS^T
+        store_bf16_64(tDPw + 64 * w, y);  // dS^T
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->ds_full[wg]);
+        mbar_arrive(&bars->ds_full);
       }
-      // ---- epilogue: warpgroup wg stores d columns [64wg, 64wg+64) of dV and dK
+      // ---- epilogue: warpgroup w stores d columns [c0, c0+64) of dV and dK
       mbar_wait_warp(&bars->acc_full, acc_ph);
       acc_ph ^= 1;
       tc_fence_after();
-      const int c0 = 64 * wg;
       const int row = un.kv_off + kj;
       const bool valid = row < un.kv_end;
       const int64_t off = (int64_t(row) * p.h_kv + un.hk) * kHeadDim + c0;
@@ -686,8 +675,8 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
     // 2. dK, dV
     if ((parts & CAD_BWD_DKDV) && !plan->kv_units.empty()) {
       kv::Params p;
-      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q, kSub);
-      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q, kSub);
+      make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
+      make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);
       make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
       make_tile_map(&p.tm_v, v, sh.kv_rows, sh.h_kv);
       p.nlse2 = lse2;

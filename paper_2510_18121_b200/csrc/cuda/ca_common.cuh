@@ -31,7 +31,7 @@ struct FwdUnit {
   int32_t n_kv;
 };
 
-constexpr int kSub = 64;  // q sub-tile rows of the dK/dV kernel
+constexpr int kSub = 128;  // q rows per dK/dV iteration
 
 // dK/dV work unit: kv tile `tile` of a KV group (the tasks sharing one KV
 // row range [kv_off, kv_end), e.g. the shards of one document on this
