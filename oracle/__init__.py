@@ -59,6 +59,7 @@ def ref_lib() -> C.CDLL:
             "ref_plan_servers": (None, [vp, P(N.f64), P(N.i64), P(N.i64), P(N.i64)]),
             "ref_plan_free": (None, [vp]),
             "ref_schedule_seconds": (N.f64, [P(N.cad_item), N.i64, N.i64, P(N.cad_sched_cfg), N.i64]),
+            "ref_grid_lookup": (N.f64, [C.c_char_p, N.f64, N.f64, N.i64, N.i64, N.i64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(h, name)

@@ -287,6 +287,21 @@ void ref_plan_servers(void* h, double* flops, int64_t* core, int64_t* sent, int6
 }
 void ref_plan_free(void* h) { delete static_cast<RefPlan*>(h); }
 
+// Loads a profiler-grid CSV with the reference's own parser
+// (grid_from_csv, P/src/cost.cpp:215-262) and returns profile_lookup at
+// (n_q, n_kv); -1 on a parse/validation error.
+double ref_grid_lookup(const char* csv, double peak, double alpha, int64_t tile, int64_t n_q,
+                       int64_t n_kv) {
+  try {
+    std::istringstream in(csv);
+    const auto g = cadsim::grid_from_csv(in, peak, alpha, tile);
+    return cadsim::profile_lookup(g, n_q, n_kv);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
 // Wall time of `reps` calls of the reference schedule() (CPU baseline).
 double ref_schedule_seconds(const cad_item* items, int64_t n, int64_t n_servers,
                             const cad_sched_cfg* cfg, int64_t reps) {
