@@ -56,11 +56,13 @@ struct cad_ca_plan {
   std::vector<cad_dev::DevTask> tasks;
   std::vector<cad_dev::FwdUnit> fwd_units;
   std::vector<cad_dev::FwdUnit> dq_units;  // nh == 1
+  std::vector<cad_dev::FwdUnit> fwd2_units;  // CTA-pair forward: nh == 4 (GQA group % 4 == 0)
   std::vector<cad_dev::KvUnit> kv_units;
   std::vector<cad_dev::KvSeg> kv_segs;
   cad_dev::DevTask* d_tasks = nullptr;
   cad_dev::FwdUnit* d_fwd = nullptr;
   cad_dev::FwdUnit* d_dq = nullptr;
+  cad_dev::FwdUnit* d_fwd2 = nullptr;
   cad_dev::KvUnit* d_kv = nullptr;
   cad_dev::KvSeg* d_segs = nullptr;
   int64_t pairs = 0;
@@ -82,5 +84,7 @@ void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, 
 // 2-D map over a [heads][rows] fp32 buffer (LSE, D): box of 128 rows x 1 head.
 void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
 void cuda_check(cudaError_t e, const char* what);
+bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
+                     cudaStream_t stream);
 
 }  // namespace cad_dev

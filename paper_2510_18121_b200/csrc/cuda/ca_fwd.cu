@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -264,8 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a = ex2(fmaf(s[c * 32 + 2 * i], p.scale_log2, neg_m));
-            const float b = ex2(fmaf(s[c * 32 + 2 * i + 1], p.scale_log2, neg_m));
+            float a = fmaf(s[c * 32 + 2 * i], p.scale_log2, neg_m);
+            float b = fmaf(s[c * 32 + 2 * i + 1], p.scale_log2, neg_m);
+            a = ex2(a);
+            b = ex2(b);
             sum += a + b;
             pk[i] = pack_bf16(a, b);
           }
@@ -322,6 +325,8 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
   return cad::guarded([&] {
     if (!plan || !q || !k || !v || !o || !lse) throw cad::DomainError("null argument");
     if (plan->fwd_units.empty()) return;
+    static const bool pair_off = std::getenv("CAD_FWD_PAIR") && std::getenv("CAD_FWD_PAIR")[0] == '0';
+    if (!pair_off && launch_fwd_pair(plan, q, k, v, o, lse, static_cast<cudaStream_t>(stream))) return;
     fwd::Params p;
     make_tile_map(&p.tm_q, q, plan->shape.q_rows, plan->shape.h_q);
     make_tile_map(&p.tm_k, k, plan->shape.kv_rows, plan->shape.h_kv);

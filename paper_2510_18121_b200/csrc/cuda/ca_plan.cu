@@ -92,6 +92,9 @@ static void build_units(cad_ca_plan& P) {
           P.fwd_units.push_back({t, i, static_cast<int16_t>(hk * group + g), static_cast<int16_t>(per_unit), n_kv});
         for (int g = 0; g < group; ++g)
           P.dq_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 1, n_kv});
+        if (group % 4 == 0)
+          for (int g = 0; g < group; g += 4)
+            P.fwd2_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 4, n_kv});
       }
     }
   }
@@ -141,6 +144,10 @@ static void build_units(cad_ca_plan& P) {
   // on the same KV head, so the K/V (fwd, dq) or Q/dO (dkdv) tiles they all
   // stream stay L2-resident; within a head the strided walk is LPT.
   std::stable_sort(P.fwd_units.begin(), P.fwd_units.end(), [group](const FwdUnit& a, const FwdUnit& b) {
+    const int ha = a.head0 / group, hb = b.head0 / group;
+    return ha != hb ? ha < hb : a.n_kv > b.n_kv;
+  });
+  std::stable_sort(P.fwd2_units.begin(), P.fwd2_units.end(), [group](const FwdUnit& a, const FwdUnit& b) {
     const int ha = a.head0 / group, hb = b.head0 / group;
     return ha != hb ? ha < hb : a.n_kv > b.n_kv;
   });
@@ -198,6 +205,7 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     upload(P->tasks, &P->d_tasks);
     upload(P->fwd_units, &P->d_fwd);
     upload(P->dq_units, &P->d_dq);
+    upload(P->fwd2_units, &P->d_fwd2);
     upload(P->kv_units, &P->d_kv);
     upload(P->kv_segs, &P->d_segs);
     *plan = P.release();
@@ -232,6 +240,7 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     cudaFree(plan->d_tasks);
     cudaFree(plan->d_fwd);
     cudaFree(plan->d_dq);
+    cudaFree(plan->d_fwd2);
     cudaFree(plan->d_kv);
     cudaFree(plan->d_segs);
     delete plan;

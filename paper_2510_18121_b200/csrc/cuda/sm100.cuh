@@ -289,12 +289,96 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// 2^x for two lanes on the FMA pipe (no MUFU): x = n + f, 2^f by a cubic
+// (max rel. error 7.5e-5, well below the bf16 rounding of P), n added to the
+// exponent. x is clamped at -126 (result ~0; -inf from masking is fine).
+__device__ __forceinline__ void exp2_fma2(float& a, float& b) {
+  a = fmaxf(a, -126.f);  // p(f) may be < 1: n >= -126 keeps the exponent sum >= 0
+  b = fmaxf(b, -126.f);
+  const uint64_t M = f2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  uint64_t x = f2(a, b), t, f, pp;
+  asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(t) : "l"(x), "l"(M));  // 1.5*2^23 + floor(x)
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(f) : "l"(t), "l"(M));  // floor(x)
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(f));  // frac in [0,1)
+  pp = ffma2(f2(0.07802334f, 0.07802334f), f, f2(0.22606643f, 0.22606643f));
+  pp = ffma2(pp, f, f2(0.69583511f, 0.69583511f));
+  pp = ffma2(pp, f, f2(0.99992490f, 0.99992490f));
+  float p0, p1, t0, t1;
+  f2_split(pp, p0, p1);
+  f2_split(t, t0, t1);
+  a = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  b = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ float4 lds4(uint32_t saddr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(saddr));
   return v;
+}
+
+// ---------------------------------------------------------------- CTA pair
+// (cluster of 2 CTAs issuing tcgen05 .cta_group::2 MMAs from the even CTA)
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address -> even CTA
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on the even CTA's copy of `bar`.
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_local(uint64_t* bar, uint32_t bytes) {
+  mbar_expect_tx(bar, bytes);
+}
+// 2-SM TMA: lands in this CTA's smem, completes tx on the even CTA's barrier.
+__device__ __forceinline__ void tma_load_3d_2sm(const void* desc, uint64_t* bar, void* dst, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_free_2sm(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kCols));
+}
+__device__ __forceinline__ void umma_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// Commit this thread's pair MMAs to the barrier at the same offset in both CTAs.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 
 // Named barrier among `threads` threads (id 1..15; 0 is __syncthreads).
