@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcad.so")
+LIB_PATH = os.environ.get("CAD_LIB_PATH") or os.path.join(_HERE, "lib", "libcad.so")
 
 i64, i32, u8, u64, f64, f32 = C.c_int64, C.c_int32, C.c_uint8, C.c_uint64, C.c_double, C.c_float
 

@@ -35,12 +35,17 @@
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
+#include "ca_softmax.cuh"
 #include "sm100.cuh"
 
 namespace cad_dev {
 
 namespace fwd {
 
+#ifndef CAD_EMU_MASK
+#define CAD_EMU_MASK 0x0000
+#endif
+constexpr uint32_t kFwdEmuMask = CAD_EMU_MASK;  // no polynomial exp2 (measured best)
 constexpr int kThreads = 384;  // softmax warpgroups 0,1 + control warpgroup (TMA, MMA, 2 idle)
 constexpr uint32_t kQOff = 0;                   // 2 x 32 KB
 constexpr uint32_t kKOff = 2 * kTileBytes;      // 2 x 32 KB
@@ -51,7 +56,7 @@ constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;  // + barriers + alignment
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_full[2], o_full[2], o_free[2];
+  uint64_t s_full[2], p_half[2], p_full[2], o_full[2], o_free[2];
   uint32_t tmem_base;
 };
 
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
       mbar_init(&bars->v_full[i], 1);
       mbar_init(&bars->v_empty[i], 1);
       mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_half[i], 128);
       mbar_init(&bars->p_full[i], 128);
       mbar_init(&bars->o_full[i], 1);
       mbar_init(&bars->o_free[i], 128);
@@ -167,16 +173,17 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
         tc_fence_after();
         for (int h = 0; h < nh; ++h) {
           dbg_mark(1, 0x400 + j * 16 + h);
-          mbar_wait(&bars->p_full[h], pph[h]);
-          dbg_mark(1, 0x500 + j * 16 + h);
-          pph[h] ^= 1;
+          mbar_wait(&bars->p_half[h], pph[h]);
           if (j == 0) {
             mbar_wait(&bars->o_free[h], fph[h] ^ 1);
             fph[h] ^= 1;
           }
           tc_fence_after();
-          issue_pv(tmem + 256 + h * 128, tmem + h * 128, tmem + h * 128 + 32,
-                   sbase + kVOff + vs * kTileBytes, j > 0);
+          issue_pv_half(tmem + 256 + h * 128, tmem + h * 128, sbase + kVOff + vs * kTileBytes, 0, j > 0);
+          mbar_wait(&bars->p_full[h], pph[h]);
+          pph[h] ^= 1;
+          tc_fence_after();
+          issue_pv_half(tmem + 256 + h * 128, tmem + h * 128 + 32, sbase + kVOff + vs * kTileBytes, 1, true);
           if (j == n - 1) {
             mma_commit(&bars->o_full[h]);
           } else {
@@ -222,62 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
         mbar_wait_warp(&bars->s_full[h], sph);
         sph ^= 1;
         tc_fence_after();
-        float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(s_tmem + c * 32, r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-        }
-        tmem_wait_ld();
-        if (j >= first_masked_tile) {
-          const int limit = pos - j * kTile;  // last visible column
-#pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c > limit) s[c] = -INFINITY;
-        }
-        float mx = s[0];
-#pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-        const float m_tile = mx * p.scale_log2;
-        if (j == 0) {
-          m = m_tile;
-        } else if (m_tile > m + 8.0f) {
-          // Lazy rescale: only when the running max grows by > 2^8.
-          const float f = ex2(m - m_tile);
-          l *= f;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(o_tmem + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-            tmem_st32(o_tmem + c * 32, r);
-          }
-          m = m_tile;
-        }
-        const float neg_m = -m;
-        float sum = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float a = fmaf(s[c * 32 + 2 * i], p.scale_log2, neg_m);
-            float b = fmaf(s[c * 32 + 2 * i + 1], p.scale_log2, neg_m);
-            a = ex2(a);
-            b = ex2(b);
-            sum += a + b;
-            pk[i] = pack_bf16(a, b);
-          }
-          tmem_st16(s_tmem + c * 16, pk);
-        }
-        l += sum;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->p_full[h]);
+        softmax_tile<kFwdEmuMask>(s_tmem, o_tmem, j == 0, j >= first_masked_tile, pos - j * kTile, p.scale_log2, m, l,
+                     [&](int half) { mbar_arrive(half ? &bars->p_full[h] : &bars->p_half[h]); });
         if (row == 0) dbg_mark(2 + h, 0x200 + j);
       }
       // ---- epilogue: O / l, LSE

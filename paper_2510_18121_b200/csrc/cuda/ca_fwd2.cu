@@ -22,13 +22,21 @@
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
+#include "ca_softmax.cuh"
 #include "sm100.cuh"
 
 namespace cad_dev {
 namespace fwd2 {
 
+#ifndef CAD_EMU_MASK
+#define CAD_EMU_MASK 0x1111
+#endif
+constexpr uint32_t kPairEmuMask = CAD_EMU_MASK;  // 4 of 16 exp2 pairs on the FMA pipe (measured best)
 constexpr int kThreads = 384;
-constexpr int kStages = 3;
+#ifndef CAD_FWD2_STAGES
+#define CAD_FWD2_STAGES 3
+#endif
+constexpr int kStages = CAD_FWD2_STAGES;
 constexpr uint32_t kHalfBytes = kTileBytes / 2;           // 16 KB: half a K or V tile
 constexpr uint32_t kQOff = 0;                             // 2 x 32 KB
 constexpr uint32_t kKOff = 2 * kTileBytes;                // kStages x 16 KB (64 kv rows x 128 d)
@@ -39,7 +47,7 @@ constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_full[2], o_full[2], o_free[2];
+  uint64_t s_full[2], p_half[2], p_full[2], o_full[2], o_free[2];
   uint32_t tmem_base;
 };
 
@@ -81,6 +89,17 @@ __device__ __forceinline__ void issue_pv_pair(uint32_t d_tmem, uint32_t p_lo, ui
   }
 }
 
+// One K-half (kv rows [64*half, 64*half+64)) of issue_pv_pair.
+__device__ __forceinline__ void issue_pv_pair_half(uint32_t d_tmem, uint32_t p, uint32_t v_smem, int half,
+                                                   bool accumulate) {
+  constexpr uint32_t idesc = idesc_bf16(256, 128, false, true);
+  if (!elect_one()) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    umma_ts_2sm(d_tmem, p + k * 8, sw128_desc(v_smem + (half * 4 + k) * 2048, kHalfBytes, 1024), idesc,
+                (accumulate || half > 0 || k > 0) ? 1u : 0u);
+}
+
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
   if (elect_one()) umma_commit_pair(bar);
   __syncwarp();
@@ -110,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_half[i], 256);
       mbar_init(&bars->p_full[i], 256);
       mbar_init(&bars->o_full[i], 1);
       mbar_init(&bars->o_free[i], 256);
@@ -182,15 +202,17 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
           mbar_wait(&bars->v_full[vs], vph);
           tc_fence_after();
           for (int h = 0; h < 2; ++h) {
-            mbar_wait(&bars->p_full[h], pph[h]);
-            pph[h] ^= 1;
+            mbar_wait(&bars->p_half[h], pph[h]);
             if (j == 0) {
               mbar_wait(&bars->o_free[h], fph[h] ^ 1);
               fph[h] ^= 1;
             }
             tc_fence_after();
-            issue_pv_pair(tmem + 256 + h * 128, tmem + h * 128, tmem + h * 128 + 32,
-                          sbase + kVOff + vs * kHalfBytes, j > 0);
+            issue_pv_pair_half(tmem + 256 + h * 128, tmem + h * 128, sbase + kVOff + vs * kHalfBytes, 0, j > 0);
+            mbar_wait(&bars->p_full[h], pph[h]);
+            pph[h] ^= 1;
+            tc_fence_after();
+            issue_pv_pair_half(tmem + 256 + h * 128, tmem + h * 128 + 32, sbase + kVOff + vs * kHalfBytes, 1, true);
             if (j == n - 1) {
               commit_pair(&bars->o_full[h]);
             } else {
@@ -233,61 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
         mbar_wait_warp(&bars->s_full[h], sph);
         sph ^= 1;
         tc_fence_after();
-        float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(s_tmem + c * 32, r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-        }
-        tmem_wait_ld();
-        if (j >= first_masked_tile) {
-          const int limit = pos - j * kTile;
-#pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c > limit) s[c] = -INFINITY;
-        }
-        float mx = s[0];
-#pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-        const float m_tile = mx * p.scale_log2;
-        if (j == 0) {
-          m = m_tile;
-        } else if (m_tile > m + 8.0f) {
-          const float f = ex2(m - m_tile);
-          l *= f;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(o_tmem + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-            tmem_st32(o_tmem + c * 32, r);
-          }
-          m = m_tile;
-        }
-        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2), nm2 = f2(-m, -m);
-        float sum = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float a, b;
-            f2_split(ffma2(f2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2), a, b);
-            a = ex2(a);
-            b = ex2(b);
-            sum += a + b;
-            pk[i] = pack_bf16(a, b);
-          }
-          tmem_st16(s_tmem + c * 16, pk);
-        }
-        l += sum;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive_leader(&bars->p_full[h]);
+        softmax_tile<kPairEmuMask>(s_tmem, o_tmem, j == 0, j >= first_masked_tile, pos - j * kTile, p.scale_log2, m, l,
+                     [&](int half) { mbar_arrive_leader(half ? &bars->p_full[h] : &bars->p_half[h]); });
       }
       mbar_wait_warp(&bars->o_full[h], oph);
       oph ^= 1;

@@ -49,6 +49,17 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t a_lo, uint32_
   }
 }
 
+// One K-half (kv rows [64*half, 64*half+64)) of issue_pv: P released in halves.
+__device__ __forceinline__ void issue_pv_half(uint32_t d_tmem, uint32_t a, uint32_t b_smem, int half,
+                                              bool accumulate) {
+  constexpr uint32_t idesc = idesc_bf16(128, 128, false, true);
+  if (!elect_one()) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    umma_ts(d_tmem, a + k * 8, sw128_desc(b_smem + (half * 4 + k) * 2048, kTileBytes / 2, 1024), idesc,
+            (accumulate || half > 0 || k > 0) ? 1u : 0u);
+}
+
 // D = A B^T with a 128-row A tile and an N-row B tile (N = 64 or 128),
 // K = 128 (d). Each operand is two SW128 planes of 64 d-values; a plane of
 // an R-row tile is R*128 bytes.

@@ -1,0 +1,21 @@
+#!/bin/bash
+# Experimental builds of the forward kernels with other CAD_EMU_MASK values
+# -> paper_2510_18121_b200/lib/variants/libcad_<name>.so (CAD_LIB_PATH=...).
+set -e
+cd "$(dirname "$0")/../paper_2510_18121_b200"
+mkdir -p lib/variants /tmp/cadvar
+# each argument: NAME:NVCC_DEFINES (comma separated), e.g. st5:CAD_FWD2_STAGES=5
+for spec in "$@"; do
+  m=${spec%%:*}; defs=$(echo "${spec#*:}" | tr ',' '\n' | sed 's/^/-D/' | tr '\n' ' ')
+  for k in ca_fwd ca_fwd2; do
+    nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
+      --expt-relaxed-constexpr $defs -c csrc/cuda/$k.cu -o /tmp/cadvar/${k}_$m.o &
+  done
+done
+wait
+for spec in "$@"; do
+  m=${spec%%:*}
+  objs=$(ls build/*.o | grep -v -E "cuda_ca_fwd2?\.o")
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o lib/variants/libcad_$m.so $objs \
+    /tmp/cadvar/ca_fwd_$m.o /tmp/cadvar/ca_fwd2_$m.o -ldl -lpthread
+done
