@@ -141,6 +141,11 @@ namespace kv {
 // P^T -> p_full; dS^T -> ds_full. MMA order: dV(i) | S^T(i+1) | dK(i) |
 // dP^T(i+1), so the tensor core runs dV(i)+S^T(i+1) while the warpgroups
 // compute dS^T(i), and dK(i)+dP^T(i+1) while they exponentiate i+1.
+#ifndef CAD_DKDV_EMU_MASK
+#define CAD_DKDV_EMU_MASK 0x1111  // 25 %: measured -4 % dK/dV time
+#endif
+// one bit per group of 4 q columns: 1 = polynomial exp2 on the FMA pipe
+constexpr uint32_t kDkdvEmuMask = CAD_DKDV_EMU_MASK;
 constexpr int kStages = 2;
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
@@ -371,10 +376,19 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           float a0, a1, a2, a3;
           f2_split(ffma2(f2(x[k], x[k + 1]), sc2, f2(nl.x, nl.y)), a0, a1);
           f2_split(ffma2(f2(x[k + 2], x[k + 3]), sc2, f2(nl.z, nl.w)), a2, a3);
-          x[k] = ex2(a0);
-          x[k + 1] = ex2(a1);
-          x[k + 2] = ex2(a2);
-          x[k + 3] = ex2(a3);
+          if ((kDkdvEmuMask >> (k / 4)) & 1) {
+            exp2_fma2(a0, a1);
+            exp2_fma2(a2, a3);
+            x[k] = a0;
+            x[k + 1] = a1;
+            x[k + 2] = a2;
+            x[k + 3] = a3;
+          } else {
+            x[k] = ex2(a0);
+            x[k + 1] = ex2(a1);
+            x[k + 2] = ex2(a2);
+            x[k + 3] = ex2(a3);
+          }
         }
         if (!full) {
 #pragma unroll
@@ -428,6 +442,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
 // ============================================================== dQ
 namespace dq {
 
+#ifndef CAD_DQ_EMU_MASK
+#define CAD_DQ_EMU_MASK 0  // measured: no gain (dQ is not MUFU-bound)
+#endif
+// one bit per group of 4 kv columns: 1 = polynomial exp2 on the FMA pipe
+constexpr uint32_t kDqEmuMask = CAD_DQ_EMU_MASK;
 constexpr uint32_t kQOff = 0;
 constexpr uint32_t kDOOff = kTileBytes;
 constexpr uint32_t kKOff = 2 * kTileBytes;  // 2 stages
@@ -437,7 +456,7 @@ constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 
 struct Bars {
   uint64_t q_full, q_empty;
-  uint64_t kv_full[2], kv_empty[2];
+  uint64_t k_full[2], v_full[2], kv_empty[2];
   uint64_t s_full, dp_full, p_read, ds_full, dq_full, dq_free;
   uint32_t tmem_base;
 };
@@ -472,7 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->v_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
     }
     mbar_init(&bars->s_full, 1);
@@ -510,13 +530,14 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         for (int j = 0; j < un.n_kv; ++j) {
           const int krow = tk.kv_off + j * kTile;
           mbar_wait(&bars->kv_empty[st], ph ^ 1);
-          mbar_expect_tx(&bars->kv_full[st], 2 * kTileBytes);
+          mbar_expect_tx(&bars->k_full[st], kTileBytes);
+          mbar_expect_tx(&bars->v_full[st], kTileBytes);
           uint8_t* k = smem + kKOff + st * kTileBytes;
           uint8_t* v = smem + kVOff + st * kTileBytes;
-          tma_load_3d(&p.tm_k, &bars->kv_full[st], k, 0, krow, hk);
-          tma_load_3d(&p.tm_k, &bars->kv_full[st], k + kTileBytes / 2, 64, krow, hk);
-          tma_load_3d(&p.tm_v, &bars->kv_full[st], v, 0, krow, hk);
-          tma_load_3d(&p.tm_v, &bars->kv_full[st], v + kTileBytes / 2, 64, krow, hk);
+          tma_load_3d(&p.tm_k, &bars->k_full[st], k, 0, krow, hk);
+          tma_load_3d(&p.tm_k, &bars->k_full[st], k + kTileBytes / 2, 64, krow, hk);
+          tma_load_3d(&p.tm_v, &bars->v_full[st], v, 0, krow, hk);
+          tma_load_3d(&p.tm_v, &bars->v_full[st], v + kTileBytes / 2, 64, krow, hk);
           if (++st == 2) { st = 0; ph ^= 1; }
         }
       }
@@ -527,11 +548,13 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         const int n = un.n_kv;
         mbar_wait(&bars->q_full, q_it & 1);
         ++q_it;
-        mbar_wait(&bars->kv_full[st], ph);
+        mbar_wait(&bars->k_full[st], ph);
         tc_fence_after();
         const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
         issue_qk(tS, sQ, sbase + kKOff + st * kTileBytes);
         mma_commit(&bars->s_full);
+        mbar_wait(&bars->v_full[st], ph);
+        tc_fence_after();
         issue_qk(tDP, sDO, sbase + kVOff + st * kTileBytes);
         mma_commit(&bars->dp_full);
         for (int j = 0; j < n; ++j) {
@@ -541,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
             if (++nst == 2) { nst = 0; nph ^= 1; }
             mbar_wait(&bars->p_read, pr_ph);
             pr_ph ^= 1;
-            mbar_wait(&bars->kv_full[nst], nph);
+            mbar_wait(&bars->k_full[nst], nph);
             tc_fence_after();
             issue_qk(tS, sQ, sbase + kKOff + nst * kTileBytes);  // S(j+1)
             mma_commit(&bars->s_full);
@@ -560,6 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           issue_pv(tDQ, ds, ds + 32, sbase + kKOff + cur * kTileBytes, j > 0);  // dQ += dS K
           mma_commit(&bars->kv_empty[cur]);
           if (j + 1 < n) {
+            mbar_wait(&bars->v_full[nst], nph);
+            tc_fence_after();
             issue_qk(tDP, sDO, sbase + kVOff + nst * kTileBytes);  // dP(j+1)
             mma_commit(&bars->dp_full);
           }
@@ -597,18 +622,29 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         tc_fence_before();
         mbar_arrive(&bars->p_read);
         const int lim = pos - (j * kTile + c0);  // last visible column
+        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2), nl2 = f2(-lse2, -lse2);
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const float e = ex2(fmaf(x[k], p.scale_log2, -lse2));
-          x[k] = k <= lim ? e : 0.f;
+        for (int k = 0; k < 64; k += 2) {
+          float a, b;
+          f2_split(ffma2(f2(x[k], x[k + 1]), sc2, nl2), a, b);
+          if ((kDqEmuMask >> (k / 4)) & 1) {
+            exp2_fma2(a, b);
+          } else {
+            a = ex2(a);
+            b = ex2(b);
+          }
+          x[k] = k <= lim ? a : 0.f;
+          x[k + 1] = k + 1 <= lim ? b : 0.f;
         }
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
         float y[64];
         load_row64(tDP + lsel + c0, y);
+        const uint64_t nd2 = f2(-dd, -dd);
 #pragma unroll
-        for (int k = 0; k < 64; ++k) y[k] = x[k] * (y[k] - dd);
+        for (int k = 0; k < 64; k += 2)
+          f2_split(fmul2(f2(x[k], x[k + 1]), fadd2(f2(y[k], y[k + 1]), nd2)), y[k], y[k + 1]);
         store_bf16_64(tDS + lsel + (j & 1) * 64 + 32 * w, y);
         tmem_wait_st();
         tc_fence_before();

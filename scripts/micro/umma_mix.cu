@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(384, 1) bench(unsigned long long* out, int ite
         if (MIX & 2) issue_qk(tmem + h * 128, sq + h * kTileBytes, sk);
       }
     }
+    if (MIX == 0) { while (clock64() - t0 < 2000000ull) {} }
     if (elect_one()) umma_commit(&bar);
     __syncwarp();
     mbar_wait(&bar, 0);
@@ -40,7 +41,9 @@ __global__ void __launch_bounds__(384, 1) bench(unsigned long long* out, int ite
     const uint32_t lane_sel = ((warp & 3) * 32) << 16;
     const uint32_t s_tmem = tmem + lane_sel + h * 128;
     float acc = 0.f;
+    unsigned long long n_ld = 0, c_ld = 0;
     while (!done) {
+      const unsigned long long ta = clock64();
       uint32_t r[32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -48,6 +51,8 @@ __global__ void __launch_bounds__(384, 1) bench(unsigned long long* out, int ite
         tmem_wait_ld();
         for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
       }
+      c_ld += clock64() - ta;
+      ++n_ld;
       if (LOAD >= 2) {
         uint32_t pk[16];
         for (int i = 0; i < 16; ++i) pk[i] = __float_as_uint(acc) + i;
@@ -57,6 +62,7 @@ __global__ void __launch_bounds__(384, 1) bench(unsigned long long* out, int ite
       }
     }
     if (acc == 12345.f) out[1] = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { out[2] = c_ld; out[3] = n_ld; }
   }
   tc_fence_before(); __syncthreads();
   if (warp == 8) tmem_free<512>(tmem);
@@ -69,16 +75,19 @@ void run(const char* name, unsigned long long* d, int iters) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   k<<<148, 384, sm>>>(d, iters);
   cudaDeviceSynchronize();
-  unsigned long long c = 0;
-  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-  const int per_it = 2 * (((MIX & 1) ? 8 : 0) + ((MIX & 2) ? 8 : 0));
-  printf("%-28s %.1f cycles/MMA (ideal 64)  err=%s\n", name, double(c) / (iters * per_it),
-         cudaGetErrorString(cudaGetLastError()));
+  unsigned long long c = 0, h[4] = {0, 0, 0, 0};
+  cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+  c = h[0];
+  const int per_it = MIX == 0 ? 1 : 2 * (((MIX & 1) ? 8 : 0) + ((MIX & 2) ? 8 : 0));
+  printf("%-28s %.1f cycles/MMA (ideal 64); 128-col tcgen05.ld row: %.0f cycles  err=%s\n", name,
+         double(c) / (iters * per_it), h[3] ? double(h[2]) / h[3] : 0.0, cudaGetErrorString(cudaGetLastError()));
+  cudaMemset(d, 0, 32);
 }
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 16);
+  cudaMalloc(&d, 32);
+  cudaMemset(d, 0, 32);
   const int iters = 2000;
   run<0, 2>("QK only", d, iters);
   run<0, 1>("PV only", d, iters);
@@ -86,6 +95,7 @@ int main() {
   run<1, 3>("PV+QK, tmem ld", d, iters);
   run<2, 3>("PV+QK, tmem ld+st", d, iters);
   run<1, 2>("QK, tmem ld", d, iters);
+  run<1, 0>("no MMA, tmem ld", d, iters);
   run<1, 1>("PV, tmem ld", d, iters);
   return 0;
 }

@@ -1,10 +1,11 @@
-"""dK/dV kernel per-iteration timeline of block 0 (debug build lib/libcad_tl.so)."""
+"""dK/dV kernel per-iteration timeline of block 0 (debug build from
+scripts/build_tl_dkdv.py). Times are cycles relative to 'S(i) ready'."""
 import ctypes as C, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
 import paper_2510_18121_b200._native as N
-N.LIB_PATH = os.path.join(ROOT, "paper_2510_18121_b200", "lib", "libcad_tl.so")
+N.LIB_PATH = os.path.join(ROOT, "paper_2510_18121_b200", "lib", "libcad_tl_dkdv.so")
 import torch
 from paper_2510_18121_b200.ca import CAPlan, CATaskRows
 T = 32768
@@ -15,19 +16,16 @@ v = torch.randn(T, 8, 128, device="cuda", dtype=torch.bfloat16)
 do = torch.randn(T, 32, 128, device="cuda", dtype=torch.bfloat16)
 o, lse = plan.forward(q, k, v)
 for _ in range(2):
-    plan.backward(q, k, v, o, lse, do)
+    plan.backward(q, k, v, o, lse, do, parts=3)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * (8 * 4096))()
+buf = (C.c_ulonglong * (24 * 8192))()
 N.lib().cad_debug_timeline(buf)
-a = np.array(buf, dtype=np.int64).reshape(8, 4096)
-n = 400
-names = ["mma:p_full", "mma:ds_full", "wg:wait_s", "wg:got_s", "wg:p_arrive", "wg:got_dp", "wg:ds_arrive"]
-t0 = a[2, 0]
-print("iter " + " ".join(f"{x:>12s}" for x in names))
-for i in range(200, 216):
-    print(f"{i:4d} " + " ".join(f"{a[e, i] - t0:12d}" for e in range(7)))
+a = np.array(buf, dtype=np.int64).reshape(24, 8192)
 it = np.arange(100, 1000)
-d = lambda e1, e2: np.median(a[e2, it] - a[e1, it])
-print("median per iteration (cycles): period", np.median(np.diff(a[3, 100:1000])))
-print("wait for S", d(2, 3), " phase1 (got S -> p_arrive)", d(3, 4), " p_arrive->got dP", d(4, 5),
-      " phase2 (got dP -> ds arrive)", d(5, 6), " p_arrive -> mma sees p", d(4, 0), " ds_arrive -> mma sees ds", d(6, 1))
+print("period", np.median(np.diff(a[3, 100:1000])))
+ev = [("wg wait S start", 2), ("wg got S", 3), ("wg P arrive", 4), ("wg got dP", 5), ("wg dS arrive", 6), ("wg1 wait S start", 14), ("wg1 got S", 15), ("wg1 P arrive", 16), ("wg1 got dP", 17), ("wg1 dS arrive", 18),
+      ("mma wait P start", 7), ("mma saw P", 0), ("mma wait in_full start", 11), ("mma saw in_full", 12),
+      ("mma issued S(i+1)", 8), ("mma wait dS start", 13), ("mma saw dS", 1), ("mma issued dK(i)", 9),
+      ("mma issued dP(i+1)", 10)]
+for name, e in ev:
+    print(f"{name:26s} {np.median(a[e, it] - a[3, it]):8.0f}")
