@@ -122,24 +122,20 @@ __global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bf
 }
 
 // ============================================================== dK / dV
-// Ping-pong over 64-row q sub-tiles: iteration i (a (head, task, sub-tile)
-// triple) uses TMEM buffer b = i & 1 and is handled by warpgroup b, so while
-// one warpgroup exponentiates sub-tile i the tensor core already computes
-// S^T/dP^T of sub-tile i+1 and the dV/dK updates of i-1.
-//   TMEM: buf b: S^T [128b, 128b+64)  dP^T [128b+64, 128b+128)
-//         dV [256,384)  dK [384,512)
-//   P^T / dS^T (bf16) overwrite the first 32 columns of S^T / dP^T.
 namespace kv {
 
 // 128-row q tiles; all four GEMMs are M=128, N=128 (the tensor core reads
 // its SS operands from shared memory at a fixed rate, so N=64 MMAs ran
 // smem-bound).
 //   TMEM: S^T [0,128)  dP^T [128,256)  dV [256,384)  dK [384,512)
-//   P^T (bf16) overwrites S^T columns: warpgroup w's 64 q columns land in
-//   [64w, 64w+32); dS^T likewise in dP^T.
-// Iteration i: S^T(i), dP^T(i) -> both warpgroups (64 q columns each):
-// P^T -> p_full; dS^T -> ds_full. MMA order: dV(i) | S^T(i+1) | dK(i) |
-// dP^T(i+1), so the tensor core runs dV(i)+S^T(i+1) while the warpgroups
+// Iteration i: S^T(i), dP^T(i) -> both warpgroups. Warpgroup w owns q
+// columns [32w, 32w+32) and [64+32w, 64+32w+32), so the two warpgroups
+// together finish q columns [0,64) (= the first K-half of dV/dK) halfway
+// through: P^T -> p_half, p_full; dS^T -> ds_half, ds_full. The bf16 P^T
+// (dS^T) of K-half h is written into the packed columns [16+64h, 48+64h)
+// of S^T (dP^T), inside the columns each warpgroup itself read.
+// MMA order: dV(i) half 0 | dV(i) half 1 | S^T(i+1) | dK(i) halves |
+// dP^T(i+1): the tensor core runs dV(i)+S^T(i+1) while the warpgroups
 // compute dS^T(i), and dK(i)+dP^T(i+1) while they exponentiate i+1.
 #ifndef CAD_DKDV_EMU_MASK
 #define CAD_DKDV_EMU_MASK 0x1111  // 25 %: measured -4 % dK/dV time
@@ -158,7 +154,7 @@ constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 struct Bars {
   uint64_t kv_full, kv_empty;
   uint64_t in_full[kStages], in_empty[kStages];
-  uint64_t s_full, dp_full, p_full, ds_full, acc_full, acc_free;
+  uint64_t s_full, dp_full, p_half, p_full, ds_half, ds_full, acc_full, acc_free;
   uint32_t tmem_base;
 };
 
@@ -171,6 +167,7 @@ struct Params {
   const KvUnit* units;
   const KvSeg* segs;
   int n_units;
+  const int32_t* sched;  // per-CTA work lists (CtaLists)
   int group;
   int h_kv;
   __nv_bfloat16* dk;
@@ -219,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
     }
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_half, 256);
     mbar_init(&bars->p_full, 256);
+    mbar_init(&bars->ds_half, 256);
     mbar_init(&bars->ds_full, 256);
     mbar_init(&bars->acc_full, 1);
     mbar_init(&bars->acc_free, 256);
@@ -241,7 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       // cp.async rather than TMA); each lane's async arrive lands on in_full
       // when its copies have (count 1 + 32).
       uint32_t kv_it = 0, st = 0, ph = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+        const int u = sched_unit(p.sched, gridDim.x, ui);
         const KvUnit un = p.units[u];
         const int krow = un.kv_off + un.tile * kTile;
         if (lane == 0) {
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       // ---------------------------------------------------------- MMA
       uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0, p_ph = 0, ds_ph = 0;
       const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+        const int u = sched_unit(p.sched, gridDim.x, ui);
         const KvUnit un = p.units[u];
         const int n = un.n_iter;
         mbar_wait(&bars->kv_full, kv_it & 1);
@@ -302,14 +303,19 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         mma_commit(&bars->dp_full);
         for (int i = 0; i < n; ++i) {
           const uint32_t cur = st;
-          mbar_wait(&bars->p_full, p_ph);
-          p_ph ^= 1;
+          // dV += P^T dO, in two K-halves (q columns [0,64) and [64,128)) as
+          // the warpgroups release them
+          mbar_wait(&bars->p_half, p_ph);
           if (i == 0) {
             mbar_wait(&bars->acc_free, (acc_it & 1) ^ 1);
             ++acc_it;
           }
           tc_fence_after();
-          issue_pv(tDV, tS, tS + 64, sDO, i > 0);  // dV += P^T dO
+          issue_pv_half(tDV, tS + 16, sDO, 0, i > 0);
+          mbar_wait(&bars->p_full, p_ph);
+          p_ph ^= 1;
+          tc_fence_after();
+          issue_pv_half(tDV, tS + 80, sDO, 1, true);
           uint32_t nQ = 0, nDO = 0;
           if (i + 1 < n) {
             if (++st == kStages) { st = 0; ph ^= 1; }
@@ -320,10 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
             issue_qk(tS, sK, nQ);  // S^T(i+1): runs after dV(i) read P^T (in order)
             mma_commit(&bars->s_full);
           }
+          mbar_wait(&bars->ds_half, ds_ph);  // dK += dS^T Q, likewise in K-halves
+          tc_fence_after();
+          issue_pv_half(tDK, tDP + 16, sQ, 0, i > 0);
           mbar_wait(&bars->ds_full, ds_ph);
           ds_ph ^= 1;
           tc_fence_after();
-          issue_pv(tDK, tDP, tDP + 64, sQ, i > 0);  // dK += dS^T Q
+          issue_pv_half(tDK, tDP + 80, sQ, 1, true);
           mma_commit(&bars->in_empty[cur]);
           if (i + 1 < n) {
             issue_qk(tDP, sV, nDO);  // dP^T(i+1)
@@ -340,13 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------------------ elementwise
-    const int w = warp >> 2;                    // q columns [64w, 64w+64)
+    const int w = warp >> 2;                    // q column chunks, see below
     const uint32_t r = (warp & 3) * 32 + lane;  // kv row within the tile
     const uint32_t lsel = ((warp & 3) * 32) << 16;
     const int c0 = 64 * w;
     const uint32_t tSw = tS + lsel, tDPw = tDP + lsel;
     uint32_t st = 0, ph = 0, s_ph = 0, dp_ph = 0, acc_ph = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+      const int u = sched_unit(p.sched, gridDim.x, ui);
       const KvUnit un = p.units[u];
       const int kj = un.tile * kTile + r;  // key index relative to kv_off
       Cursor c;
@@ -354,70 +364,118 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs, p.group)) {
         const DevTask tk = p.tasks[p.segs[c.seg].task];
         const int shift = tk.kv_len - tk.n_q;
-        const int q0 = c.qt * kTile + c0;  // query index of this thread's column 0
         mbar_wait_warp(&bars->in_full[st], ph);
-        const uint32_t s_nlse = smem_u32(rows + st * 256 + c0), s_nd = s_nlse + 512;
+        const uint32_t s_nlse = smem_u32(rows + st * 256), s_nd = s_nlse + 512;
         if (++st == kStages) { st = 0; ph ^= 1; }
         mbar_wait_warp(&bars->s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
+        // Warpgroup w owns q columns [32w, 32w+32) (chunk 0) and
+        // [64+32w, 64+32w+32) (chunk 1): both warpgroups finish chunk 0 first,
+        // which completes q columns [0,64) = the first K-half of dV/dK.
         float x[64];
-        load_row64(tSw + c0, x);
-        // column c visible iff kj <= shift + q0 + c and q0 + c < n_q; this
-        // warpgroup's 64 columns are mask-free (CTA-uniform) when the tile's
-        // last kv row is visible from column 0 and all columns are queries.
-        const int lo = kj - shift - q0;
-        const int hi = tk.n_q - q0;
-        const bool full = (un.tile * kTile + kTile - 1 - shift - q0) <= 0 && hi >= 64;
-        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
+        {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(tSw + 32 * w, r0);
+          tmem_ld32(tSw + 64 + 32 * w, r1);
+          tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 64; k += 4) {
-          const float4 nl = lds4(s_nlse + 4 * k);
-          float a0, a1, a2, a3;
-          f2_split(ffma2(f2(x[k], x[k + 1]), sc2, f2(nl.x, nl.y)), a0, a1);
-          f2_split(ffma2(f2(x[k + 2], x[k + 3]), sc2, f2(nl.z, nl.w)), a2, a3);
-          if ((kDkdvEmuMask >> (k / 4)) & 1) {
-            exp2_fma2(a0, a1);
-            exp2_fma2(a2, a3);
-            x[k] = a0;
-            x[k + 1] = a1;
-            x[k + 2] = a2;
-            x[k + 3] = a3;
-          } else {
-            x[k] = ex2(a0);
-            x[k + 1] = ex2(a1);
-            x[k + 2] = ex2(a2);
-            x[k + 3] = ex2(a3);
+          for (int k = 0; k < 32; ++k) {
+            x[k] = __uint_as_float(r0[k]);
+            x[32 + k] = __uint_as_float(r1[k]);
           }
         }
-        if (!full) {
+        const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
 #pragma unroll
-          for (int k = 0; k < 64; ++k) x[k] = (k >= lo && k < hi) ? x[k] : 0.f;
+        for (int ch = 0; ch < 2; ++ch) {
+          // column k of the chunk is visible iff kj <= shift + qb + k and
+          // qb + k < n_q; the chunk is mask-free (warp-uniform) when the
+          // tile's last kv row is visible from its column 0 and all of its
+          // columns are queries.
+          const int qb = c.qt * kTile + 64 * ch + 32 * w;
+          const int lo = kj - shift - qb;
+          const int hi = tk.n_q - qb;
+          const bool full = (un.tile * kTile + kTile - 1 - shift - qb) <= 0 && hi >= 32;
+          float* xc = x + 32 * ch;
+          const uint32_t s_l = s_nlse + 4 * (64 * ch + 32 * w);
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float4 nl = lds4(s_l + 4 * k);
+            float a0, a1, a2, a3;
+            f2_split(ffma2(f2(xc[k], xc[k + 1]), sc2, f2(nl.x, nl.y)), a0, a1);
+            f2_split(ffma2(f2(xc[k + 2], xc[k + 3]), sc2, f2(nl.z, nl.w)), a2, a3);
+            if ((kDkdvEmuMask >> (k / 4)) & 1) {
+              exp2_fma2(a0, a1);
+              exp2_fma2(a2, a3);
+              xc[k] = a0;
+              xc[k + 1] = a1;
+              xc[k + 2] = a2;
+              xc[k + 3] = a3;
+            } else {
+              xc[k] = ex2(a0);
+              xc[k + 1] = ex2(a1);
+              xc[k + 2] = ex2(a2);
+              xc[k + 3] = ex2(a3);
+            }
+          }
+          if (!full) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) xc[k] = (k >= lo && k < hi) ? xc[k] : 0.f;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) pk[k] = pack_bf16(xc[2 * k], xc[2 * k + 1]);
+          // P^T (bf16) inside this warpgroup's own S^T columns: K-half ch
+          // is the 32 packed columns at 16 + 64 ch (WG0 first, then WG1)
+          tmem_st16(tSw + 16 + 64 * ch + 16 * w, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(ch ? &bars->p_full : &bars->p_half);
         }
-        store_bf16_64(tSw + 64 * w, x);  // P^T: WG0 -> cols [0,32), WG1 -> [64,96)
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->p_full);
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
         float y[64];
-        load_row64(tDPw + c0, y);
+        {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(tDPw + 32 * w, r0);
+          tmem_ld32(tDPw + 64 + 32 * w, r1);
+          tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 64; k += 4) {
-          const float4 nd = lds4(s_nd + 4 * k);
-          f2_split(fmul2(f2(x[k], x[k + 1]), fadd2(f2(y[k], y[k + 1]), f2(nd.x, nd.y))), y[k], y[k + 1]);
-          f2_split(fmul2(f2(x[k + 2], x[k + 3]), fadd2(f2(y[k + 2], y[k + 3]), f2(nd.z, nd.w))), y[k + 2],
-                   y[k + 3]);
+          for (int k = 0; k < 32; ++k) {
+            y[k] = __uint_as_float(r0[k]);
+            y[32 + k] = __uint_as_float(r1[k]);
+          }
         }
-        if (!full) {
 #pragma unroll
-          for (int k = 0; k < 64; ++k) y[k] = (k >= lo && k < hi) ? y[k] : 0.f;
+        for (int ch = 0; ch < 2; ++ch) {
+          const int qb = c.qt * kTile + 64 * ch + 32 * w;
+          const int lo = kj - shift - qb;
+          const int hi = tk.n_q - qb;
+          const bool full = (un.tile * kTile + kTile - 1 - shift - qb) <= 0 && hi >= 32;
+          const float* xc = x + 32 * ch;
+          float* yc = y + 32 * ch;
+          const uint32_t s_d = s_nd + 4 * (64 * ch + 32 * w);
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float4 nd = lds4(s_d + 4 * k);
+            f2_split(fmul2(f2(xc[k], xc[k + 1]), fadd2(f2(yc[k], yc[k + 1]), f2(nd.x, nd.y))), yc[k],
+                     yc[k + 1]);
+            f2_split(fmul2(f2(xc[k + 2], xc[k + 3]), fadd2(f2(yc[k + 2], yc[k + 3]), f2(nd.z, nd.w))),
+                     yc[k + 2], yc[k + 3]);
+          }
+          if (!full) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) yc[k] = (k >= lo && k < hi) ? yc[k] : 0.f;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) pk[k] = pack_bf16(yc[2 * k], yc[2 * k + 1]);
+          tmem_st16(tDPw + 16 + 64 * ch + 16 * w, pk);  // dS^T (bf16), same layout
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(ch ? &bars->ds_full : &bars->ds_half);
         }
-        store_bf16_64(tDPw + 64 * w, y);  // dS^T
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bars->ds_full);
       }
       // ---- epilogue: warpgroup w stores d columns [c0, c0+64) of dV and dK
       mbar_wait_warp(&bars->acc_full, acc_ph);
@@ -466,6 +524,7 @@ struct Params {
   const DevTask* tasks;
   const FwdUnit* units;
   int n_units;
+  const int32_t* sched;  // per-CTA work lists (CtaLists)
   int group;
   int h_q;
   const float* lse2;   // -LSE * log2(e), [h_q][pitch]
@@ -515,7 +574,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 8 && lane == 0) {
       uint32_t q_it = 0, st = 0, ph = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+        const int u = sched_unit(p.sched, gridDim.x, ui);
         const FwdUnit un = p.units[u];
         const DevTask tk = p.tasks[un.task];
         const int hk = un.head0 / p.group;
@@ -543,7 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
       }
     } else if (warp == 9) {
       uint32_t q_it = 0, st = 0, ph = 0, dq_it = 0, pr_ph = 0, ds_ph = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+        const int u = sched_unit(p.sched, gridDim.x, ui);
         const FwdUnit un = p.units[u];
         const int n = un.n_kv;
         mbar_wait(&bars->q_full, q_it & 1);
@@ -603,7 +664,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
     const uint32_t lsel = ((warp & 3) * 32) << 16;
     const int c0 = 64 * w;
     uint32_t s_ph = 0, dp_ph = 0, dq_ph = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+      const int u = sched_unit(p.sched, gridDim.x, ui);
       const FwdUnit un = p.units[u];
       const DevTask tk = p.tasks[un.task];
       const int shift = tk.kv_len - tk.n_q;
@@ -636,6 +698,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           x[k] = k <= lim ? a : 0.f;
           x[k + 1] = k + 1 <= lim ? b : 0.f;
         }
+        // finish every exponential before waiting for dP: otherwise the
+        // compiler sinks part of them past the wait, onto the critical path
+        // dS(j) -> dQ(j) -> dP(j+1) -> dS(j+1)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) asm volatile("" : "+f"(x[k]));
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
@@ -722,13 +789,14 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.units = plan->d_kv;
       p.segs = plan->d_segs;
       p.n_units = static_cast<int>(plan->kv_units.size());
+      p.sched = plan->sched_kv.d;
       p.group = sh.h_q / sh.h_kv;
       p.h_kv = sh.h_kv;
       p.dk = static_cast<__nv_bfloat16*>(dk);
       p.dv = static_cast<__nv_bfloat16*>(dv);
       p.scale = sh.softmax_scale;
       p.scale_log2 = sh.softmax_scale * kLog2e;
-      const int grid = plan->grid(p.n_units);
+      const int grid = plan->sched_kv.G;
       kv::ca_bwd_dkdv_kernel<<<grid, kThreads, kv::kSmemBytes, s>>>(p);
       cuda_check(cudaGetLastError(), "ca_bwd_dkdv launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv");
@@ -743,6 +811,7 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.tasks = plan->d_tasks;
       p.units = plan->d_dq;
       p.n_units = static_cast<int>(plan->dq_units.size());
+      p.sched = plan->sched_dq.d;
       p.group = sh.h_q / sh.h_kv;
       p.h_q = sh.h_q;
       p.lse2 = lse2;
@@ -751,7 +820,7 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.pitch = pitch;
       p.scale = sh.softmax_scale;
       p.scale_log2 = sh.softmax_scale * kLog2e;
-      const int grid = plan->grid(p.n_units);
+      const int grid = plan->sched_dq.G;
       dq::ca_bwd_dq_kernel<<<grid, kThreads, dq::kSmemBytes, s>>>(p);
       cuda_check(cudaGetLastError(), "ca_bwd_dq launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq");

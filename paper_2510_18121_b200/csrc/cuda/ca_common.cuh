@@ -49,6 +49,19 @@ struct KvSeg {
   int32_t task, qt_lo, qt_hi;
 };
 
+// Static per-CTA work lists: CTA (or CTA pair) c runs units
+// list[off[c] .. off[c+1]) in order. Stored on the device as one array:
+// off[0..G] followed by list.
+struct CtaLists {
+  int G = 0;
+  std::vector<int32_t> host;  // off (G + 1) then list
+  int32_t* d = nullptr;
+};
+
+__device__ __forceinline__ int32_t sched_begin(const int32_t* sc, int c) { return sc[c]; }
+__device__ __forceinline__ int32_t sched_end(const int32_t* sc, int c) { return sc[c + 1]; }
+__device__ __forceinline__ int32_t sched_unit(const int32_t* sc, int G, int32_t i) { return sc[G + 1 + i]; }
+
 }  // namespace cad_dev
 
 struct cad_ca_plan {
@@ -71,8 +84,10 @@ struct cad_ca_plan {
   int max_ctas = 0;  // 0: one persistent CTA per SM
   int grid(int64_t units) const {
     const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms) : num_sms;
-    return static_cast<int>(std::min<int64_t>(units, cap));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, cap)));
   }
+  // LPT work lists per kernel for the current grid (rebuilt by set_max_ctas)
+  cad_dev::CtaLists sched_fwd, sched_fwd2, sched_dq, sched_kv;
 };
 
 namespace cad_dev {

@@ -65,6 +65,7 @@ struct Params {
   const DevTask* tasks;
   const FwdUnit* units;
   int n_units;
+  const int32_t* sched;  // per-CTA work lists (CtaLists)
   int h_q;
   int group;  // h_q / h_kv
   __nv_bfloat16* o;
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+        const int u = sched_unit(p.sched, gridDim.x, ui);
         const FwdUnit un = p.units[u];
         const DevTask tk = p.tasks[un.task];
         const int hk = un.head0 / p.group;  // the KV head shared by the unit's query heads
@@ -151,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
     // ------------------------------------------------------------ MMA issuer
     uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
     uint32_t pph[2] = {0, 0}, fph[2] = {0, 0};
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+      const int u = sched_unit(p.sched, gridDim.x, ui);
       const FwdUnit un = p.units[u];
       const int n = un.n_kv, nh = un.nh;
       dbg_mark(1, 0x100);
@@ -215,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
     const uint32_t s_tmem = tmem + lane_sel + h * 128;
     const uint32_t o_tmem = tmem + lane_sel + 256 + h * 128;
     uint32_t sph = 0, oph = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
+      const int u = sched_unit(p.sched, gridDim.x, ui);
       const FwdUnit un = p.units[u];
       if (h >= un.nh) continue;
       const DevTask tk = p.tasks[un.task];
@@ -287,6 +291,7 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
     p.tasks = plan->d_tasks;
     p.units = plan->d_fwd;
     p.n_units = static_cast<int>(plan->fwd_units.size());
+    p.sched = plan->sched_fwd.d;
     p.h_q = plan->shape.h_q;
     p.group = plan->shape.h_q / plan->shape.h_kv;
     p.o = static_cast<__nv_bfloat16*>(o);
@@ -300,7 +305,7 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
                  "cudaFuncSetAttribute(fwd)");
       attr_set = true;
     }
-    const int grid = plan->grid(p.n_units);
+    const int grid = plan->sched_fwd.G;
     fwd::ca_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(p);
     cuda_check(cudaGetLastError(), "ca_fwd launch");
   });

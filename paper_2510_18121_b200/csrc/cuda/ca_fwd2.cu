@@ -56,6 +56,7 @@ struct Params {
   const DevTask* tasks;
   const FwdUnit* units;  // nh == 4: heads head0..head0+3
   int n_units;
+  const int32_t* sched;  // per-CTA work lists (CtaLists)
   int h_q;
   int group;
   __nv_bfloat16* o;
@@ -148,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
       // ---------------------------------------------------------- producer (both CTAs)
       if (lane == 0) {
         uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
-        for (int u = pair; u < p.n_units; u += n_pairs) {
+        for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
+          const int u = sched_unit(p.sched, n_pairs, ui);
           const FwdUnit un = p.units[u];
           const DevTask tk = p.tasks[un.task];
           const int hk = un.head0 / p.group;
@@ -184,7 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
       // ---------------------------------------------------------- MMA (even CTA)
       uint32_t q_it = 0, ks = 0, kph = 0, vs = 0, vph = 0;
       uint32_t pph[2] = {0, 0}, fph[2] = {0, 0};
-      for (int u = pair; u < p.n_units; u += n_pairs) {
+      for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
+        const int u = sched_unit(p.sched, n_pairs, ui);
         const FwdUnit un = p.units[u];
         const int n = un.n_kv;
         mbar_wait(&bars->q_full, q_it & 1);
@@ -243,7 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
     const uint32_t s_tmem = tmem + lane_sel + h * 128;
     const uint32_t o_tmem = tmem + lane_sel + 256 + h * 128;
     uint32_t sph = 0, oph = 0;
-    for (int u = pair; u < p.n_units; u += n_pairs) {
+    for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
+      const int u = sched_unit(p.sched, n_pairs, ui);
       const FwdUnit un = p.units[u];
       const DevTask tk = p.tasks[un.task];
       const int shift = tk.kv_len - tk.n_q;
@@ -305,6 +309,7 @@ bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, cons
   p.tasks = plan->d_tasks;
   p.units = plan->d_fwd2;
   p.n_units = static_cast<int>(plan->fwd2_units.size());
+  p.sched = plan->sched_fwd2.d;
   p.h_q = plan->shape.h_q;
   p.group = plan->shape.h_q / plan->shape.h_kv;
   p.o = static_cast<__nv_bfloat16*>(o);
@@ -318,7 +323,7 @@ bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, cons
                "cudaFuncSetAttribute(fwd2)");
     attr_set = true;
   }
-  const int pairs = std::max(1, std::min<int>(p.n_units, plan->grid(1 << 30) / 2));
+  const int pairs = plan->sched_fwd2.G;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(fwd2::kThreads);

@@ -7,9 +7,11 @@
 // tiles 0..n_kv-1 (tiles entirely above the diagonal are never visited).
 // Backward: one unit per (task, 128-row kv tile, KV head, pair of query
 // heads); it walks q tiles from the first one that can see the kv tile.
-// Units are sorted by KV head, then by length, longest first, so the
-// persistent CTAs' strided walk shares L2-resident tiles and ends each head
-// with its short units (LPT).
+// Units are sorted by KV head, then by length, longest first, and dealt to
+// the persistent CTAs greedily (each unit to the CTA with the least work so
+// far, LPT): concurrently running CTAs stay on the same KV head, sharing
+// L2-resident tiles, and every CTA ends within about one short unit of the
+// others.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -20,6 +22,7 @@
 #include <mutex>
 #include <type_traits>
 #include <numeric>
+#include <queue>
 #include <string>
 
 #include "../host/cad_status.hpp"
@@ -160,6 +163,50 @@ static void build_units(cad_ca_plan& P) {
   });
 }
 
+// Greedy LPT deal of units (in their sorted order) over G CTAs.
+static void deal(CtaLists& L, const std::vector<int64_t>& cost, int G) {
+  G = std::max(1, G);
+  std::vector<std::vector<int32_t>> per(G);
+  using Slot = std::pair<int64_t, int>;  // (load, cta): ties go to the lower CTA
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  for (int c = 0; c < G; ++c) heap.push({0, c});
+  for (size_t u = 0; u < cost.size(); ++u) {
+    Slot s = heap.top();
+    heap.pop();
+    per[s.second].push_back(static_cast<int32_t>(u));
+    s.first += cost[u];
+    heap.push(s);
+  }
+  L.G = G;
+  L.host.assign(1, 0);
+  for (int c = 0; c < G; ++c) L.host.push_back(L.host.back() + static_cast<int32_t>(per[c].size()));
+  for (int c = 0; c < G; ++c) L.host.insert(L.host.end(), per[c].begin(), per[c].end());
+  cudaFree(L.d);
+  L.d = nullptr;
+  cuda_check(cudaMalloc(reinterpret_cast<void**>(&L.d), L.host.size() * sizeof(int32_t)), "cudaMalloc(sched)");
+  cuda_check(cudaMemcpy(L.d, L.host.data(), L.host.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+             "cudaMemcpy(sched)");
+}
+
+// Per-unit cost in tile iterations, plus the unit's fixed prologue/epilogue.
+static void build_schedules(cad_ca_plan& P) {
+  std::vector<int64_t> c;
+  auto fwd_cost = [&](const std::vector<FwdUnit>& v) {
+    c.clear();
+    for (const FwdUnit& u : v) c.push_back(int64_t(u.n_kv) + 1);
+    return c;
+  };
+  deal(P.sched_fwd, fwd_cost(P.fwd_units), P.grid(P.fwd_units.size()));
+  // CTA pairs: half the grid, one list per pair
+  deal(P.sched_fwd2, fwd_cost(P.fwd2_units),
+       std::max<int>(1, std::min<int64_t>(P.fwd2_units.size(), P.grid(1 << 30) / 2)));
+  deal(P.sched_dq, fwd_cost(P.dq_units), P.grid(P.dq_units.size()));
+  c.clear();
+  const int group = P.shape.h_q / P.shape.h_kv;
+  for (const KvUnit& u : P.kv_units) c.push_back(int64_t(u.n_iter) + 2 * group);
+  deal(P.sched_kv, c, P.grid(P.kv_units.size()));
+}
+
 }  // namespace cad_dev
 
 using cad_dev::cuda_check;
@@ -208,6 +255,7 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     upload(P->fwd2_units, &P->d_fwd2);
     upload(P->kv_units, &P->d_kv);
     upload(P->kv_segs, &P->d_segs);
+    cad_dev::build_schedules(*P);
     *plan = P.release();
   });
 }
@@ -231,6 +279,7 @@ int cad_ca_plan_set_max_ctas(cad_ca_plan* plan, int max_ctas) {
   return cad::guarded([&] {
     if (!plan || max_ctas < 0) throw cad::DomainError("bad argument");
     plan->max_ctas = max_ctas;
+    cad_dev::build_schedules(*plan);
   });
 }
 
@@ -243,6 +292,8 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     cudaFree(plan->d_fwd2);
     cudaFree(plan->d_kv);
     cudaFree(plan->d_segs);
+    for (cad_dev::CtaLists* L : {&plan->sched_fwd, &plan->sched_fwd2, &plan->sched_dq, &plan->sched_kv})
+      cudaFree(L->d);
     delete plan;
   });
 }
