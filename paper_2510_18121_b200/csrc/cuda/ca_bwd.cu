@@ -505,18 +505,32 @@ namespace dq {
 #endif
 // one bit per group of 4 kv columns: 1 = polynomial exp2 on the FMA pipe
 constexpr uint32_t kDqEmuMask = CAD_DQ_EMU_MASK;
+// K tiles are read twice per iteration (S(j) and, later, dQ(j)), V once
+// (dP(j)): a 3-deep K ring and a 2-deep V ring, each slot freed as soon as
+// its last reader completes.
+constexpr int kKStages = 3, kVStages = 2;
 constexpr uint32_t kQOff = 0;
 constexpr uint32_t kDOOff = kTileBytes;
-constexpr uint32_t kKOff = 2 * kTileBytes;  // 2 stages
-constexpr uint32_t kVOff = 4 * kTileBytes;  // 2 stages
-constexpr uint32_t kBarOff = 6 * kTileBytes;
+constexpr uint32_t kKOff = 2 * kTileBytes;
+constexpr uint32_t kVOff = kKOff + kKStages * kTileBytes;
+constexpr uint32_t kBarOff = kVOff + kVStages * kTileBytes;
 constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+static_assert(kSmemBytes <= 232448, "dQ shared memory");
 
 struct Bars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[2], v_full[2], kv_empty[2];
-  uint64_t s_full, dp_full, p_read, ds_full, dq_full, dq_free;
+  uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
+  uint64_t s_full, dp_full, p_read, dp_read, ds_full, dq_full, dq_free;
   uint32_t tmem_base;
+};
+
+// Slot index + phase of a ring of N stages.
+template <int N>
+struct Ring {
+  uint32_t i = 0, ph = 0;
+  __device__ void next() {
+    if (++i == N) { i = 0; ph ^= 1; }
+  }
 };
 
 struct Params {
@@ -549,14 +563,18 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
     tma_prefetch(&p.tm_do);
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+    }
+    for (int i = 0; i < kVStages; ++i) {
       mbar_init(&bars->v_full[i], 1);
-      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
     }
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->p_read, 256);
+    mbar_init(&bars->dp_read, 256);
     mbar_init(&bars->ds_full, 256);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 256);
@@ -573,7 +591,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 8 && lane == 0) {
-      uint32_t q_it = 0, st = 0, ph = 0;
+      uint32_t q_it = 0;
+      Ring<kKStages> kr;
+      Ring<kVStages> vr;
       for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
         const int u = sched_unit(p.sched, gridDim.x, ui);
         const FwdUnit un = p.units[u];
@@ -589,49 +609,64 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         tma_load_3d(&p.tm_do, &bars->q_full, smem + kDOOff + kTileBytes / 2, 64, qrow, un.head0);
         for (int j = 0; j < un.n_kv; ++j) {
           const int krow = tk.kv_off + j * kTile;
-          mbar_wait(&bars->kv_empty[st], ph ^ 1);
-          mbar_expect_tx(&bars->k_full[st], kTileBytes);
-          mbar_expect_tx(&bars->v_full[st], kTileBytes);
-          uint8_t* k = smem + kKOff + st * kTileBytes;
-          uint8_t* v = smem + kVOff + st * kTileBytes;
-          tma_load_3d(&p.tm_k, &bars->k_full[st], k, 0, krow, hk);
-          tma_load_3d(&p.tm_k, &bars->k_full[st], k + kTileBytes / 2, 64, krow, hk);
-          tma_load_3d(&p.tm_v, &bars->v_full[st], v, 0, krow, hk);
-          tma_load_3d(&p.tm_v, &bars->v_full[st], v + kTileBytes / 2, 64, krow, hk);
-          if (++st == 2) { st = 0; ph ^= 1; }
+          mbar_wait(&bars->k_empty[kr.i], kr.ph ^ 1);
+          mbar_expect_tx(&bars->k_full[kr.i], kTileBytes);
+          uint8_t* k = smem + kKOff + kr.i * kTileBytes;
+          tma_load_3d(&p.tm_k, &bars->k_full[kr.i], k, 0, krow, hk);
+          tma_load_3d(&p.tm_k, &bars->k_full[kr.i], k + kTileBytes / 2, 64, krow, hk);
+          kr.next();
+          mbar_wait(&bars->v_empty[vr.i], vr.ph ^ 1);
+          mbar_expect_tx(&bars->v_full[vr.i], kTileBytes);
+          uint8_t* v = smem + kVOff + vr.i * kTileBytes;
+          tma_load_3d(&p.tm_v, &bars->v_full[vr.i], v, 0, krow, hk);
+          tma_load_3d(&p.tm_v, &bars->v_full[vr.i], v + kTileBytes / 2, 64, krow, hk);
+          vr.next();
         }
       }
     } else if (warp == 9) {
-      uint32_t q_it = 0, st = 0, ph = 0, dq_it = 0, pr_ph = 0, ds_ph = 0;
+      // Per iteration j: S(j+1) as soon as the S(j) rows are in registers,
+      // dP(j+1) as soon as the dP(j) rows are, then dQ(j) once dS(j) is in
+      // TMEM (dS is double-buffered, so dS(j+1) can be written meanwhile).
+      uint32_t q_it = 0, dq_it = 0, pr_ph = 0, dr_ph = 0, ds_ph = 0;
+      Ring<kKStages> kr;
+      Ring<kVStages> vr;
       for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
         const int u = sched_unit(p.sched, gridDim.x, ui);
         const FwdUnit un = p.units[u];
         const int n = un.n_kv;
         mbar_wait(&bars->q_full, q_it & 1);
         ++q_it;
-        mbar_wait(&bars->k_full[st], ph);
-        tc_fence_after();
         const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
-        issue_qk(tS, sQ, sbase + kKOff + st * kTileBytes);
-        mma_commit(&bars->s_full);
-        mbar_wait(&bars->v_full[st], ph);
+        mbar_wait(&bars->k_full[kr.i], kr.ph);
         tc_fence_after();
-        issue_qk(tDP, sDO, sbase + kVOff + st * kTileBytes);
+        issue_qk(tS, sQ, sbase + kKOff + kr.i * kTileBytes);  // S(0)
+        mma_commit(&bars->s_full);
+        mbar_wait(&bars->v_full[vr.i], vr.ph);
+        tc_fence_after();
+        issue_qk(tDP, sDO, sbase + kVOff + vr.i * kTileBytes);  // dP(0)
         mma_commit(&bars->dp_full);
+        mma_commit(&bars->v_empty[vr.i]);
+        vr.next();
         for (int j = 0; j < n; ++j) {
-          const uint32_t cur = st;
-          uint32_t nst = st, nph = ph;
+          const uint32_t kcur = kr.i;
+          kr.next();
+          mbar_wait(&bars->p_read, pr_ph);
+          pr_ph ^= 1;
           if (j + 1 < n) {
-            if (++nst == 2) { nst = 0; nph ^= 1; }
-            mbar_wait(&bars->p_read, pr_ph);
-            pr_ph ^= 1;
-            mbar_wait(&bars->k_full[nst], nph);
+            mbar_wait(&bars->k_full[kr.i], kr.ph);
             tc_fence_after();
-            issue_qk(tS, sQ, sbase + kKOff + nst * kTileBytes);  // S(j+1)
+            issue_qk(tS, sQ, sbase + kKOff + kr.i * kTileBytes);  // S(j+1)
             mma_commit(&bars->s_full);
-          } else {
-            mbar_wait(&bars->p_read, pr_ph);
-            pr_ph ^= 1;
+          }
+          mbar_wait(&bars->dp_read, dr_ph);
+          dr_ph ^= 1;
+          if (j + 1 < n) {
+            mbar_wait(&bars->v_full[vr.i], vr.ph);
+            tc_fence_after();
+            issue_qk(tDP, sDO, sbase + kVOff + vr.i * kTileBytes);  // dP(j+1)
+            mma_commit(&bars->dp_full);
+            mma_commit(&bars->v_empty[vr.i]);
+            vr.next();
           }
           mbar_wait(&bars->ds_full, ds_ph);
           ds_ph ^= 1;
@@ -641,20 +676,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           }
           tc_fence_after();
           const uint32_t ds = tDS + (j & 1) * 64;
-          issue_pv(tDQ, ds, ds + 32, sbase + kKOff + cur * kTileBytes, j > 0);  // dQ += dS K
-          mma_commit(&bars->kv_empty[cur]);
-          if (j + 1 < n) {
-            mbar_wait(&bars->v_full[nst], nph);
-            tc_fence_after();
-            issue_qk(tDP, sDO, sbase + kVOff + nst * kTileBytes);  // dP(j+1)
-            mma_commit(&bars->dp_full);
-          }
-          st = nst;
-          ph = nph;
+          issue_pv(tDQ, ds, ds + 32, sbase + kKOff + kcur * kTileBytes, j > 0);  // dQ += dS K
+          mma_commit(&bars->k_empty[kcur]);
         }
         mma_commit(&bars->dq_full);
         mma_commit(&bars->q_empty);
-        if (++st == 2) { st = 0; ph ^= 1; }
       }
     }
   } else {
@@ -698,16 +724,13 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
           x[k] = k <= lim ? a : 0.f;
           x[k + 1] = k + 1 <= lim ? b : 0.f;
         }
-        // finish every exponential before waiting for dP: otherwise the
-        // compiler sinks part of them past the wait, onto the critical path
-        // dS(j) -> dQ(j) -> dP(j+1) -> dS(j+1)
-#pragma unroll
-        for (int k = 0; k < 64; ++k) asm volatile("" : "+f"(x[k]));
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
         float y[64];
         load_row64(tDP + lsel + c0, y);
+        tc_fence_before();
+        mbar_arrive(&bars->dp_read);
         const uint64_t nd2 = f2(-dd, -dd);
 #pragma unroll
         for (int k = 0; k < 64; k += 2)
