@@ -4,9 +4,12 @@ Workload: BASELINE config 3 shape (Llama-3-8B CA, 32 Q / 8 KV heads), 65536
 tokens per GPU (512K at 8 GPUs), pretrain_upsampled documents (seed 1),
 placed sequentially; CA-tasks sharded by the bit-exact scheduler; per layer
 the Q/KV dispatch, CA fwd, O/LSE return, dO dispatch, CA bwd, dQ and dK/dV
-return run over NCCL all-to-allv with ping/pong halves (dispatch.py).
-Scaling is weak (fixed tokens per GPU). Times are CUDA events on the compute
-stream, max over ranks.
+return run with ping/pong halves (dispatch.py) over copy-engine pushes
+(CUDA IPC, default; CAD_TRANSPORT=nccl for NCCL all-to-allv). A step is
+CAD_LAYERS (default 1) stacked CA layers, forward then backward, with the
+identity between layers, so transfers of one layer overlap the neighbouring
+layer's CA compute. Scaling is weak (fixed tokens per GPU). Times are CUDA
+events on the compute stream, max over ranks.
 """
 import json
 import os
@@ -51,7 +54,12 @@ def run(args, metric, load_peaks, ClockSampler):
     dist.broadcast_object_list(obj, src=0)
     comm = D.Comm(obj[0], rank, world)
     transport = os.environ.get("CAD_TRANSPORT", "ce")
-    reserve = int(os.environ.get("CAD_RESERVE_SMS", "0" if transport == "ce" else "8"))
+    # copy-engine transport: row pushes by copy engines ('ce') or by an SM
+    # copy kernel on CAD_COPY_CTAS SMs kept free of CA work ('sm')
+    copy_mode = os.environ.get("CAD_COPY", "ce")
+    copy_ctas = int(os.environ.get("CAD_COPY_CTAS", "4"))
+    reserve = int(os.environ.get("CAD_RESERVE_SMS", (str(copy_ctas) if copy_mode == "sm" else "0")
+                                 if transport == "ce" else "8"))
     dev = torch.device("cuda", local)
     layer = D.DistCALayer(lp, comm, dev, reserve_sms=reserve)
     H = lp.home_rows
@@ -69,8 +77,12 @@ def run(args, metric, load_peaks, ClockSampler):
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)
     comp = torch.cuda.current_stream(dev)
+    # stacked CA layers per step (copy-engine transport): the dispatch of
+    # layer l+1 and the return of layer l overlap the other half's CA
+    layers = int(os.environ.get("CAD_LAYERS", "1")) if transport == "ce" else 1
     if transport == "ce":
-        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq)
+        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq,
+                               layers=layers, copy_mode=copy_mode, copy_ctas=copy_ctas)
 
     def step(mode="pingpong"):
         layer.step(q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode=mode)
@@ -90,7 +102,9 @@ def run(args, metric, load_peaks, ClockSampler):
     launches = layer.launches + (layer.ce.launches if layer.ce is not None else 0) + 2 * args.steps
     ms_compute, my_compute = _timed(lambda: step("compute"), max(2, args.steps // 2), comp)
     ms_comm, _ = _timed(lambda: step("comm"), max(2, args.steps // 2), comp)
-    ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)  # NCCL, no overlap
+    ms_serial = None
+    if transport != "ce":
+        ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)  # NCCL, no overlap
     ms_signal = None
     if layer.ce is not None:
         ms_signal, _ = _timed(lambda: step("signal"), max(2, args.steps // 2), comp)
@@ -111,11 +125,22 @@ def run(args, metric, load_peaks, ClockSampler):
 
     e2e()
     ms_e2e, _ = _timed(e2e, max(2, args.steps // 2), comp)
+    trace = None
+    if os.environ.get("CAD_TRACE") and layer.ce is not None:
+        # per-kernel flag waits on the compute stream in one ping-pong step
+        layer.ce.trace = []
+        step()
+        torch.cuda.synchronize()
+        tr = layer.ce.trace
+        layer.ce.trace = None
+        t0 = [x for x in tr if x[0] == "F"][0][3]
+        trace = sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
+                         round(b.elapsed_time(c), 2)) for (k, l, h, a, b, c) in tr], key=lambda r: r[3])
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_, hdo_)) * world
     d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv)) * world
 
     pairs = lp.server_pairs()
-    wire = sum(sum(hp.remote_send_bytes) for hp in lp.halves)
+    wire = sum(sum(hp.remote_send_bytes) for hp in lp.halves) * layers
     wire_fwd = sum(hp.remote_send_bytes[0] * 2 + hp.remote_send_bytes[1] for hp in lp.halves)
     stats = torch.tensor([pairs, my_compute, wire, my_ms], dtype=torch.float64, device=dev)
     allst = [torch.zeros_like(stats) for _ in range(world)]
@@ -124,7 +149,7 @@ def run(args, metric, load_peaks, ClockSampler):
     if rank == 0:
         peak, peak_sus, peak_kind = load_peaks()
         total_pairs = allst[:, 0].sum()
-        flops = 14.0 * 128 * shape.h_q * total_pairs
+        flops = 14.0 * 128 * shape.h_q * total_pairs * layers
         value = flops / ms / 1e9
         # hidden = 1 - (T_pingpong - T_signal) / T_comm_only (the
         # reference's signal/ping-pong modes, P/tests/acceptance.cpp:272-290)
@@ -143,13 +168,16 @@ def run(args, metric, load_peaks, ClockSampler):
             "config": {"workload": f"BASELINE config 3 shape: Llama-3-8B CA (32 Q / 8 KV), {per_gpu} tokens per GPU "
                                    f"({per_gpu * world} total), pretrain_upsampled seed 1, scheduler-sharded, "
                                    f"{'copy-engine (CUDA IPC) pushes' if transport == 'ce' else 'NCCL all-to-allv'} dispatch/return, "
-                                   "ping-pong halves, one layer fwd+bwd",
+                                   f"ping-pong halves, {layers} stacked CA layer(s) fwd+bwd per step "
+                                   "(identity between layers)",
+                       "layers_per_step": layers,
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
                        "parallelism": f"CA servers x{world} (scheduler sharding)",
-                       "transport": transport, "reserve_sms_for_comm": reserve},
+                       "transport": transport, "copy_mode": copy_mode if transport == "ce" else None,
+                       "reserve_sms_for_comm": reserve},
             "per_gpu_tflops": value / world, "pct_bf16_peak": value / world / peak,
-            "tokens_per_s": per_gpu * world / (ms / 1e3),
+            "tokens_per_s": per_gpu * world * layers / (ms / 1e3),  # token-layers (fwd+bwd) per second
             "imbalance": {"max_over_mean_pairs": float(allst[:, 0].max() / allst[:, 0].mean()),
                           "max_over_mean_ca_time": float(allst[:, 1].max() / allst[:, 1].mean()),
                           "naive_max_over_mean_pairs": max(naive_pairs) / (sum(naive_pairs) / world)},
@@ -167,6 +195,10 @@ def run(args, metric, load_peaks, ClockSampler):
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if trace is not None:
+            out["trace_rank0"] = {"columns": ["kind", "layer", "half", "t_ms", "flag_wait_ms", "kernel_ms"],
+                                  "rows": trace,
+                                  "flag_wait_total_ms": round(sum(r[4] for r in trace if r[0] in "FB"), 2)}
         print(json.dumps(out))
     comm.close()
     dist.barrier()

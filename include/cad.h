@@ -424,6 +424,18 @@ int cad_copy_runs(const cad_run* runs, int64_t n, const void* src, void* dst,
 int cad_copy_runs_cols(const cad_run* runs, int64_t n, const float* src,
                        int64_t src_rows, float* dst, int64_t dst_rows,
                        int32_t heads, void* stream);
+/* SM-driven copy of a list of byte ranges (device array of cad_span; dst
+ * may be a peer mapping, written over NVLink by loads/stores): one launch of
+ * n_ctas CTAs for the whole list, 16-byte vectors where src, dst and size
+ * are 16-byte aligned, 4-byte words otherwise (sizes must be multiples of
+ * 4). Used instead of copy-engine memcpys when the CA kernels' L2 traffic
+ * starves the copy engines. */
+typedef struct cad_span {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+} cad_span;
+int cad_copy_spans(const cad_span* spans_dev, int64_t n, int32_t n_ctas, void* stream);
 /* GPU-side flags: write a 32-bit value once prior stream work is done, and
  * make a stream wait until a (local) flag is >= value. */
 int cad_stream_write_u32(void* addr, uint32_t value, void* stream);

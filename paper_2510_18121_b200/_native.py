@@ -152,6 +152,7 @@ SIGNATURES = {
     "cad_ipc_open": (C.c_int, [P(u8), P(vp)]),
     "cad_ipc_close": (C.c_int, [vp]),
     "cad_copy_runs": (C.c_int, [vp, i64, vp, vp, i64, vp]),
+    "cad_copy_spans": (C.c_int, [vp, i64, i32, vp]),
     "cad_copy_runs_cols": (C.c_int, [vp, i64, vp, i64, vp, i64, i32, vp]),
     "cad_stream_write_u32": (C.c_int, [vp, C.c_uint32, vp]),
     "cad_stream_wait_u32": (C.c_int, [vp, C.c_uint32, vp]),

@@ -185,6 +185,48 @@ struct cad_comm {
   int32_t rank = 0, world = 1;
 };
 
+namespace cad_dev {
+
+// Grid-stride copy of a span list: span i is cut into 64 KB chunks, chunk c
+// of the concatenation goes to CTA c % gridDim.x. 16-byte vectors when the
+// span is 16-byte aligned, 4-byte words otherwise.
+__global__ void __launch_bounds__(512) copy_spans_kernel(const cad_span* spans, int64_t n) {
+  constexpr int64_t kChunk = 65536;
+  int64_t base = 0;  // first chunk index of span i
+  for (int64_t i = 0; i < n; ++i) {
+    const cad_span sp = spans[i];
+    const int64_t chunks = (sp.bytes + kChunk - 1) / kChunk;
+    int64_t c = (blockIdx.x - base % gridDim.x + gridDim.x) % gridDim.x;  // my first chunk of this span
+    for (; c < chunks; c += gridDim.x) {
+      const int64_t off = c * kChunk;
+      const int64_t len = min(kChunk, sp.bytes - off);
+      const char* src = static_cast<const char*>(sp.src) + off;
+      char* dst = static_cast<char*>(sp.dst) + off;
+      if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | len) & 15) == 0) {
+        const int4* s4 = reinterpret_cast<const int4*>(src);
+        int4* d4 = reinterpret_cast<int4*>(dst);
+        const int64_t nv = len / 16;
+        int64_t k = threadIdx.x;
+        for (; k + 3 * 512 < nv; k += 4 * 512) {
+          const int4 a = s4[k], b = s4[k + 512], c2 = s4[k + 1024], d = s4[k + 1536];
+          d4[k] = a;
+          d4[k + 512] = b;
+          d4[k + 1024] = c2;
+          d4[k + 1536] = d;
+        }
+        for (; k < nv; k += 512) d4[k] = s4[k];
+      } else {
+        const int* s1 = reinterpret_cast<const int*>(src);
+        int* d1 = reinterpret_cast<int*>(dst);
+        for (int64_t k = threadIdx.x; k < len / 4; k += 512) d1[k] = s1[k];
+      }
+    }
+    base += chunks;
+  }
+}
+
+}  // namespace cad_dev
+
 extern "C" {
 
 int cad_comm_unique_id(uint8_t id[CAD_UNIQUE_ID_BYTES]) {
@@ -346,6 +388,15 @@ int cad_copy_runs(const cad_run* runs, int64_t n, const void* src, void* dst, in
                                           static_cast<size_t>(r.n_rows * row_bytes), cudaMemcpyDeviceToDevice, s),
                           "cudaMemcpyAsync(run)");
     }
+  });
+}
+
+int cad_copy_spans(const cad_span* spans, int64_t n, int32_t n_ctas, void* stream) {
+  return cad::guarded([&] {
+    if (n == 0) return;
+    if (!spans || n_ctas < 1) throw cad::DomainError("bad argument");
+    cad_dev::copy_spans_kernel<<<n_ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(spans, n);
+    cad_dev::cuda_check(cudaGetLastError(), "copy_spans launch");
   });
 }
 

@@ -164,6 +164,7 @@ class DistCALayer:
         self.comm_stream = torch.cuda.Stream(device=device)
         self.halves = []
         bf = dict(dtype=torch.bfloat16, device=device)
+        self._bf = bf
         max_bytes = 1
         for hp in lp.halves:
             plan = CAPlan(hp.tasks, self.hq, self.hkv, max(1, hp.q_rows), max(1, hp.kv_rows)) if hp.tasks else None
@@ -186,9 +187,24 @@ class DistCALayer:
                 max_bytes = max(max_bytes, x.n_send * self.q_row, x.n_recv * self.q_row)
             self.halves.append(half)
         self.send_buf = torch.empty(max_bytes, dtype=torch.uint8, device=device)
+        self._max_bytes = max_bytes
         self.recv_buf = torch.empty(max_bytes, dtype=torch.uint8, device=device)
         self.launches = 0
         self.ce = None
+
+    def alloc_halves(self):
+        """Another set of per-half server buffers (a further layer's
+        activations), sharing this layer's plans and row lists."""
+        out = []
+        bf = self._bf
+        for H in self.halves:
+            qr, kr = H["q"].shape[0], H["k"].shape[0]
+            out.append({"q": torch.empty(qr, self.hq, self.d, **bf), "k": torch.empty(kr, self.hkv, self.d, **bf),
+                        "v": torch.empty(kr, self.hkv, self.d, **bf), "o": torch.empty(qr, self.hq, self.d, **bf),
+                        "lse": torch.empty(self.hq, qr, dtype=torch.float32, device=self.dev),
+                        "do": torch.empty(qr, self.hq, self.d, **bf), "dq": torch.empty(qr, self.hq, self.d, **bf),
+                        "dk": torch.empty(kr, self.hkv, self.d, **bf), "dv": torch.empty(kr, self.hkv, self.d, **bf)})
+        return out
 
     # ---------------------------------------------------------------- exchange
     def _exchange(self, dx: _DevXfer, src: torch.Tensor, dst: torch.Tensor, row_bytes: int, stream,
@@ -242,26 +258,36 @@ class DistCALayer:
         self._exchange(H["x"][XFER_KV_RET], H["dk"], dk_acc, self.kv_row, stream, mode="add")
         self._exchange(H["x"][XFER_KV_RET], H["dv"], dv_acc, self.kv_row, stream, mode="add")
 
-    def ca_fwd(self, h, stream):
-        H = self.halves[h]
-        if H["plan"] is not None:
-            H["plan"].forward(H["q"], H["k"], H["v"], H["o"], H["lse"], stream=stream)
+    def _bufs(self, h, layer):
+        if layer == 0:
+            return self.halves[h]
+        return self.ce.lbufs[layer][h]
+
+    def ca_fwd(self, h, stream, layer: int = 0):
+        plan = self.halves[h]["plan"]
+        H = self._bufs(h, layer)
+        if plan is not None:
+            plan.forward(H["q"], H["k"], H["v"], H["o"], H["lse"], stream=stream)
             self.launches += 1
 
-    def ca_bwd(self, h, stream):
-        H = self.halves[h]
-        if H["plan"] is not None:
+    def ca_bwd(self, h, stream, layer: int = 0):
+        plan = self.halves[h]["plan"]
+        H = self._bufs(h, layer)
+        if plan is not None:
             H["dk"].zero_()
             H["dv"].zero_()
-            H["plan"].backward(H["q"], H["k"], H["v"], H["o"], H["lse"], H["do"], H["dq"], H["dk"], H["dv"],
-                               H["ws"], stream=stream)
+            plan.backward(H["q"], H["k"], H["v"], H["o"], H["lse"], H["do"], H["dq"], H["dk"], H["dv"],
+                          self.halves[h]["ws"], stream=stream)
             self.launches += 3
 
     # ---------------------------------------------------------------- step
-    def use_copy_engines(self, all_plans: List[LayerPlan], o, lse, dq):
+    def use_copy_engines(self, all_plans: List[LayerPlan], o, lse, dq, layers: int = 1, copy_mode: str = "ce",
+                         copy_ctas: int = 4):
         """Switch the exchanges to the copy-engine transport (CUDA IPC pushes);
-        o/lse/dq become the registered home output buffers of every step."""
-        self.ce = CETransport(self, all_plans, o, lse, dq)
+        o/lse/dq become the registered home output buffers of every step.
+        layers > 1: every step runs that many stacked CA layers (see
+        CETransport.step)."""
+        self.ce = CETransport(self, all_plans, o, lse, dq, layers, copy_mode, copy_ctas)
 
     def step(self, q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode: str = "pingpong"):
         """One layer fwd+bwd. mode: 'pingpong' (comm of one half under CA of
@@ -280,10 +306,13 @@ class DistCALayer:
         dk_acc.zero_()
         dv_acc.zero_()
         if mode == "compute":
-            for h in (0, 1):
-                self.ca_fwd(h, comp)
-            for h in (0, 1):
-                self.ca_bwd(h, comp)
+            n_layers = self.ce.layers if getattr(self, "ce", None) is not None else 1
+            for l in range(n_layers):
+                for h in (0, 1):
+                    self.ca_fwd(h, comp, l)
+            for l in range(n_layers - 1, -1, -1):
+                for h in (0, 1):
+                    self.ca_bwd(h, comp, l)
             return
         if mode == "comm":
             for h in (0, 1):
@@ -371,6 +400,7 @@ def _split(counts, arr):
 class _RunList:
     def __init__(self, runs: np.ndarray):
         self.n = len(runs)
+        self.arr_np = np.asarray(runs, dtype=np.int64).reshape(-1, 3)
         self.arr = (N.cad_run * max(1, self.n))()
         for i, (a, b, c) in enumerate(runs.tolist()):
             self.arr[i] = N.cad_run(a, b, c)
@@ -380,7 +410,8 @@ class CETransport:
     """Row pushes over CUDA IPC for one DistCALayer. Needs every rank's
     LayerPlan (all ranks build them deterministically)."""
 
-    def __init__(self, layer: "DistCALayer", all_plans: List[LayerPlan], o, lse, dq):
+    def __init__(self, layer: "DistCALayer", all_plans: List[LayerPlan], o, lse, dq, layers: int = 1,
+                 copy_mode: str = "ce", copy_ctas: int = 4):
         import torch.distributed as dist
         self.layer, self.plans = layer, all_plans
         lp = layer.lp
@@ -388,21 +419,31 @@ class CETransport:
         self.W, self.me = W, me
         dev = layer.dev
         self.o, self.lse, self.dq = o, lse, dq
-        # dK/dV partial staging per half (rows in this rank's KV_RET recv order)
+        self.layers = max(1, layers)
+        # Server-side buffers per layer (layer 0 = the DistCALayer's halves):
+        # a multi-layer step keeps every layer's forward activations on the
+        # server for its backward, as a real stack would.
+        self.lbufs = [layer.halves] + [layer.alloc_halves() for _ in range(1, self.layers)]
+        # dK/dV partial staging per layer and half (rows in this rank's
+        # KV_RET recv order)
         self.stage = []
-        for hp in lp.halves:
-            n = max(1, hp.xfers[XFER_KV_RET].n_recv)
-            self.stage.append({"dk": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
-                               "dv": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
-                               "idx": layer.halves[lp.halves.index(hp)]["x"][XFER_KV_RET].recv_idx})
+        for _ in range(self.layers):
+            st = []
+            for h, hp in enumerate(lp.halves):
+                n = max(1, hp.xfers[XFER_KV_RET].n_recv)
+                st.append({"dk": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
+                           "dv": torch.empty(n, layer.hkv, layer.d, dtype=torch.bfloat16, device=dev),
+                           "idx": layer.halves[h]["x"][XFER_KV_RET].recv_idx})
+            self.stage.append(st)
         self.flags = torch.zeros(16 * W, dtype=torch.int32, device=dev)
         # buffers peers write into, exported once
         local = {"flags": self.flags, "o": o, "lse": lse, "dq": dq}
-        for h, H in enumerate(layer.halves):
-            for n_ in ("q", "k", "v", "do"):
-                local[f"{n_}{h}"] = H[n_]
-            local[f"sdk{h}"] = self.stage[h]["dk"]
-            local[f"sdv{h}"] = self.stage[h]["dv"]
+        for l in range(self.layers):
+            for h, H in enumerate(self.lbufs[l]):
+                for n_ in ("q", "k", "v", "do"):
+                    local[f"{n_}{h}_{l}"] = H[n_]
+                local[f"sdk{h}_{l}"] = self.stage[l][h]["dk"]
+                local[f"sdv{h}_{l}"] = self.stage[l][h]["dv"]
         mine = {}
         for name, t in local.items():
             hb = (N.u8 * 64)()
@@ -442,6 +483,13 @@ class CETransport:
         self.gen = 0
         self.launches = 0
         self.move = True
+        self.trace = None  # list of (kind, layer, half, ev_before_wait, ev_after_wait, ev_done) when tracing
+        # 'ce': copy-engine memcpys; 'sm': one copy kernel per transfer on
+        # copy_ctas SMs left free by the CA kernels (the CA kernels' L2
+        # traffic starves the copy engines)
+        self.copy_mode = copy_mode
+        self.copy_ctas = copy_ctas
+        self._spans = {}
 
     def close(self):
         for b in self.bases:
@@ -453,27 +501,73 @@ class CETransport:
         return self.peer[p]["flags"] + 4 * ((kind * 2 + h) * self.W + src)
 
     def _signal(self, kind, h, stream):
+        self._signal_v(kind, h, stream, self.gen)
+
+    def _signal_v(self, kind, h, stream, value):
         for p in range(self.W):
-            check(lib().cad_stream_write_u32(self._flag(p, kind, h, self.me), self.gen, stream.cuda_stream))
+            check(lib().cad_stream_write_u32(self._flag(p, kind, h, self.me), value, stream.cuda_stream))
 
     def _await(self, kind, h, stream, value=None):
         v = self.gen if value is None else value
         for src in range(self.W):
             check(lib().cad_stream_wait_u32(self._flag(self.me, kind, h, src), v, stream.cuda_stream))
 
-    def _push(self, h, x, src, dst_name, row_bytes, stream):
-        if not self.move:
+    def _copy(self, h, x, src_ptr, dst_name, row_bytes, stream):
+        """Push rows of exchange x (half h) from src_ptr into every peer's
+        buffer dst_name: copy-engine memcpys, or one SM copy kernel on the
+        reserved SMs (copy_mode 'sm')."""
+        if self.copy_mode == "sm":
+            key = (h, x, src_ptr, dst_name, row_bytes)
+            spans = self._spans.get(key)
+            if spans is None:
+                rows = []
+                for p in range(self.W):
+                    rl = self.runs[(h, x, p)]
+                    dst = self.peer[p][dst_name]
+                    for r in rl.arr_np:
+                        rows.append((src_ptr + int(r[0]) * row_bytes, dst + int(r[1]) * row_bytes,
+                                     int(r[2]) * row_bytes))
+                spans = torch.tensor(rows if rows else [(0, 0, 0)], dtype=torch.int64).to(self.layer.dev)
+                spans = (spans, len(rows))
+                self._spans[key] = spans
+            if spans[1]:
+                check(lib().cad_copy_spans(spans[0].data_ptr(), spans[1], self.copy_ctas, stream.cuda_stream))
+                self.launches += 1
             return
         for p in range(self.W):
             rl = self.runs[(h, x, p)]
             if rl.n:
-                check(lib().cad_copy_runs(rl.arr, rl.n, src.data_ptr(), self.peer[p][dst_name], row_bytes,
+                check(lib().cad_copy_runs(rl.arr, rl.n, src_ptr, self.peer[p][dst_name], row_bytes,
                                           stream.cuda_stream))
+
+    def _push(self, h, x, src, dst_name, row_bytes, stream):
+        if not self.move:
+            return
+        self._copy(h, x, src.data_ptr(), dst_name, row_bytes, stream)
 
     def _push_lse(self, h, src_lse, stream):
         if not self.move:
             return
         L = self.layer
+        if self.copy_mode == "sm":
+            key = ("lse", h, src_lse.data_ptr())
+            spans = self._spans.get(key)
+            if spans is None:
+                rows = []
+                sr = src_lse.shape[1]
+                for p in range(self.W):
+                    rl = self.runs[(h, XFER_O_RET, p)]
+                    dr = self.plans[p].home_rows
+                    for r in rl.arr_np:
+                        for hd in range(L.hq):
+                            rows.append((src_lse.data_ptr() + 4 * (hd * sr + int(r[0])),
+                                         self.peer[p]["lse"] + 4 * (hd * dr + int(r[1])), 4 * int(r[2])))
+                spans = (torch.tensor(rows if rows else [(0, 0, 0)], dtype=torch.int64).to(L.dev), len(rows))
+                self._spans[key] = spans
+            if spans[1]:
+                check(lib().cad_copy_spans(spans[0].data_ptr(), spans[1], self.copy_ctas, stream.cuda_stream))
+                self.launches += 1
+            return
         for p in range(self.W):
             rl = self.runs[(h, XFER_O_RET, p)]
             if rl.n:
@@ -482,10 +576,21 @@ class CETransport:
                                                self.peer[p]["lse"], dst_rows, L.hq, stream.cuda_stream))
 
     def step(self, q, k, v, do, dk_acc, dv_acc, compute: bool = True, move: bool = True):
-        """One layer. compute=False moves the same rows without running the
-        CA kernels (comm-only time); move=False keeps every flag/ordering but
-        skips the row copies (the reference's 'signal' mode, sim.hpp:14-18,
-        where each transfer shrinks to a message)."""
+        """One step = self.layers CA layers, forward then backward.
+        compute=False moves the same rows without running the CA kernels
+        (comm-only time); move=False keeps every flag/ordering but skips the
+        row copies (the reference's 'signal' mode, sim.hpp:14-18, where each
+        transfer shrinks to a message).
+
+        Between layers the context-independent part of the model is the
+        identity: layer l+1's Q/K/V of half h leave home once every server
+        has returned O(h, l), and layer l's dO of half h once every dQ/dK/dV
+        partial of layer l+1 is back. So with L > 1 the ping-pong also runs
+        across layers: the return of half h of layer l and the dispatch of
+        half h of layer l+1 hide under CA(1-h) (the reference hides them under
+        the CI layers, P/src/sim.cpp:69-125)."""
+        if self.layers > 1:
+            return self._step_layers(q, k, v, do, dk_acc, dv_acc, compute, move)
         L = self.layer
         self.move = move
         comp = torch.cuda.current_stream(L.dev)
@@ -502,9 +607,9 @@ class CETransport:
         fwd_done, bwd_done = [], []
 
         def dispatch_qkv(h):
-            self._push(h, XFER_Q, q, f"q{h}", L.q_row, comm)
-            self._push(h, XFER_KV, k, f"k{h}", L.kv_row, comm)
-            self._push(h, XFER_KV, v, f"v{h}", L.kv_row, comm)
+            self._push(h, XFER_Q, q, f"q{h}_0", L.q_row, comm)
+            self._push(h, XFER_KV, k, f"k{h}_0", L.kv_row, comm)
+            self._push(h, XFER_KV, v, f"v{h}_0", L.kv_row, comm)
             self._signal(F_QKV, h, comm)
 
         def ca(h, fwd):
@@ -519,7 +624,7 @@ class CETransport:
         ca(0, True)
         dispatch_qkv(1)
         for h in (0, 1):
-            self._push(h, XFER_Q, do, f"do{h}", L.q_row, comm)
+            self._push(h, XFER_Q, do, f"do{h}_0", L.q_row, comm)
             self._signal(F_DO, h, comm)
         ca(1, True)
         for h in (0, 1):
@@ -533,15 +638,15 @@ class CETransport:
             comm.wait_event(bwd_done[h])
             H = L.halves[h]
             self._push(h, XFER_O_RET, H["dq"], "dq", L.q_row, comm)
-            self._push(h, XFER_KV_RET, H["dk"], f"sdk{h}", L.kv_row, comm)
-            self._push(h, XFER_KV_RET, H["dv"], f"sdv{h}", L.kv_row, comm)
+            self._push(h, XFER_KV_RET, H["dk"], f"sdk{h}_0", L.kv_row, comm)
+            self._push(h, XFER_KV_RET, H["dv"], f"sdv{h}_0", L.kv_row, comm)
             self._signal(F_G, h, comm)
         dk_acc.zero_()
         dv_acc.zero_()
         for h in (0, 1):
             self._await(F_O, h, comp)
             self._await(F_G, h, comp)
-            st = self.stage[h]
+            st = self.stage[0][h]
             n = L.lp.halves[h].xfers[XFER_KV_RET].n_recv
             check(lib().cad_scatter_add_bf16(st["dk"].data_ptr(), st["idx"].data_ptr(), n, L.hkv * L.d,
                                              dk_acc.data_ptr(), comp.cuda_stream))
@@ -549,3 +654,150 @@ class CETransport:
                                              dv_acc.data_ptr(), comp.cuda_stream))
             self.launches += 2
         self._signal(F_DONE, 0, comp)
+
+    # ------------------------------------------------------------ L layers
+    def _push_l(self, h, x, src, name, l, row_bytes, stream):
+        if not self.move:
+            return
+        self._copy(h, x, src.data_ptr(), f"{name}{h}_{l}", row_bytes, stream)
+
+    def _step_layers(self, q, k, v, do, dk_acc, dv_acc, compute, move):
+        L = self.layer
+        NL = self.layers
+        self.move = move
+        comp = torch.cuda.current_stream(L.dev)
+        comm = L.comm_stream
+        # flag values of this step, increasing in issue order (waits are >=):
+        # forward layer l -> g0 + 1 + l, backward layer l -> g0 + 2 NL - l,
+        # F_DONE -> g0 + 2 NL
+        g0 = self.gen
+        self.gen += 2 * NL
+        start = torch.cuda.Event()
+        start.record(comp)
+        comm.wait_event(start)
+        self._await(F_DONE, 0, comm, g0)  # every peer finished the previous step
+
+        def gl(l):
+            return g0 + 1 + l
+
+        def gb(l):
+            return g0 + 2 * NL - l
+
+        def tr_comm(tag, l, h, fn):
+            if self.trace is None:
+                return fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(comm)
+            fn()
+            b.record(comm)
+            self.trace.append((tag, l, h, a, a, b))
+
+        def dispatch_qkv(h, l):
+            def f():
+                self._push_l(h, XFER_Q, q, "q", l, L.q_row, comm)
+                self._push_l(h, XFER_KV, k, "k", l, L.kv_row, comm)
+                self._push_l(h, XFER_KV, v, "v", l, L.kv_row, comm)
+            tr_comm("D", l, h, f)
+            self._signal_v(F_QKV, h, comm, gl(l))
+
+        def dispatch_do(h, l):
+            tr_comm("dO", l, h, lambda: self._push_l(h, XFER_Q, do, "do", l, L.q_row, comm))
+            self._signal_v(F_DO, h, comm, gb(l))
+
+        def ca(h, l, fwd):
+            if self.trace is not None:
+                e_pre = torch.cuda.Event(enable_timing=True)
+                e_pre.record(comp)
+            self._await(F_QKV if fwd else F_DO, h, comp, gl(l) if fwd else gb(l))
+            if self.trace is not None:
+                e_go = torch.cuda.Event(enable_timing=True)
+                e_go.record(comp)
+            H = self.lbufs[l][h]
+            if compute and L.halves[h]["plan"] is not None:
+                plan = L.halves[h]["plan"]
+                if fwd:
+                    plan.forward(H["q"], H["k"], H["v"], H["o"], H["lse"], stream=comp)
+                    L.launches += 1
+                else:
+                    H["dk"].zero_()
+                    H["dv"].zero_()
+                    plan.backward(H["q"], H["k"], H["v"], H["o"], H["lse"], H["do"], H["dq"], H["dk"], H["dv"],
+                                  L.halves[h]["ws"], stream=comp)
+                    L.launches += 3
+            e = torch.cuda.Event(enable_timing=self.trace is not None)
+            e.record(comp)
+            if self.trace is not None:
+                self.trace.append(("F" if fwd else "B", l, h, e_pre, e_go, e))
+            return e
+
+        def ret_o(h, l, ev):
+            comm.wait_event(ev)
+            H = self.lbufs[l][h]
+            if self.trace is not None:
+                ta = torch.cuda.Event(enable_timing=True)
+                ta.record(comm)
+            if self.move:
+                self._copy(h, XFER_O_RET, H["o"].data_ptr(), "o", L.q_row, comm)
+                self._push_lse(h, H["lse"], comm)
+            if self.trace is not None:
+                tb = torch.cuda.Event(enable_timing=True)
+                tb.record(comm)
+                self.trace.append(("R", l, h, ta, ta, tb))
+            self._signal_v(F_O, h, comm, gl(l))
+
+        def ret_g(h, l, ev):
+            comm.wait_event(ev)
+            H = self.lbufs[l][h]
+            if self.trace is not None:
+                ta = torch.cuda.Event(enable_timing=True)
+                ta.record(comm)
+            if self.move:
+                self._copy(h, XFER_O_RET, H["dq"].data_ptr(), "dq", L.q_row, comm)
+            self._push_l(h, XFER_KV_RET, H["dk"], "sdk", l, L.kv_row, comm)
+            self._push_l(h, XFER_KV_RET, H["dv"], "sdv", l, L.kv_row, comm)
+            if self.trace is not None:
+                tb = torch.cuda.Event(enable_timing=True)
+                tb.record(comm)
+                self.trace.append(("G", l, h, ta, ta, tb))
+            self._signal_v(F_G, h, comm, gb(l))
+
+        # forward: comm D(0,0) D(1,0) | R(0,l) D(0,l+1) | R(1,l) D(1,l+1) | ...
+        #          comp      F(0,0) F(1,0) F(0,1) F(1,1) ...
+        dispatch_qkv(0, 0)
+        ev0 = ca(0, 0, True)
+        dispatch_qkv(1, 0)
+        dispatch_do(0, NL - 1)  # the loss gradient of the top layer
+        dispatch_do(1, NL - 1)
+        pend = [ev0, None]
+        pend[1] = ca(1, 0, True)
+        for l in range(NL):
+            for h in (0, 1):
+                ret_o(h, l, pend[h])
+                if l + 1 < NL:
+                    self._await(F_O, h, comm, gl(l))  # identity CI: O(h, l) home -> Q/K/V(h, l+1)
+                    dispatch_qkv(h, l + 1)
+                    pend[h] = ca(h, l + 1, True)
+        # backward, top layer first: comm G(0,l) dO(0,l-1) | G(1,l) dO(1,l-1) ...
+        pend = [ca(0, NL - 1, False), ca(1, NL - 1, False)]
+        dk_acc.zero_()
+        dv_acc.zero_()
+        for l in range(NL - 1, -1, -1):
+            for h in (0, 1):
+                ret_g(h, l, pend[h])
+                if l > 0:
+                    self._await(F_G, h, comm, gb(l))  # identity CI: dQ(h, l) home -> dO(h, l-1)
+                    dispatch_do(h, l - 1)
+                    pend[h] = ca(h, l - 1, False)
+        for h in (0, 1):
+            self._await(F_O, h, comp, gl(NL - 1))
+            self._await(F_G, h, comp, gb(0))
+        for l in range(NL - 1, -1, -1):
+            for h in (0, 1):
+                st = self.stage[l][h]
+                n = L.lp.halves[h].xfers[XFER_KV_RET].n_recv
+                check(lib().cad_scatter_add_bf16(st["dk"].data_ptr(), st["idx"].data_ptr(), n, L.hkv * L.d,
+                                                 dk_acc.data_ptr(), comp.cuda_stream))
+                check(lib().cad_scatter_add_bf16(st["dv"].data_ptr(), st["idx"].data_ptr(), n, L.hkv * L.d,
+                                                 dv_acc.data_ptr(), comp.cuda_stream))
+                self.launches += 2
+        self._signal_v(F_DONE, 0, comp, g0 + 2 * NL)

@@ -46,9 +46,12 @@ def main():
     dk_acc = torch.zeros(H, shape.h_kv, 128, device=dev)
     dv_acc = torch.zeros_like(dk_acc)
     transport = os.environ.get("CAD_TRANSPORT", "ce")
+    # CAD_LAYERS > 1: stacked layers per step; every layer sees the same
+    # inputs, so O/LSE/dQ match one layer and dK/dV sum over the layers
+    layers = int(os.environ.get("CAD_LAYERS", "1")) if transport == "ce" else 1
     if transport == "ce":
         plans = [D.LayerPlan(lengths, world, r, shape) for r in range(world)]
-        layer.use_copy_engines(plans, o, lse, dq)
+        layer.use_copy_engines(plans, o, lse, dq, layers=layers, copy_mode=os.environ.get("CAD_COPY", "ce"))
     for mode in ("pingpong", "serial", "pingpong"):
         o.zero_(); dq.zero_(); lse.zero_()
         layer.step(home["q"], home["k"], home["v"], home["do"], o, lse, dq, dk_acc, dv_acc, mode=mode)
@@ -65,9 +68,9 @@ def main():
         "o": (o.float() - ro[rows_d].float()).abs().max().item(),
         "lse": (lse - rlse[:, rows_d]).abs().max().item(),
         "dq": (dq.float() - rdq[rows_d].float()).abs().max().item(),
-        "dk": (dk_acc - rdk[rows_d].float()).abs().max().item(),
-        "dv": (dv_acc - rdv[rows_d].float()).abs().max().item(),
-        "migrations": lp.plan.migrations, "rank": rank, "transport": transport,
+        "dk": (dk_acc / layers - rdk[rows_d].float()).abs().max().item(),
+        "dv": (dv_acc / layers - rdv[rows_d].float()).abs().max().item(),
+        "migrations": lp.plan.migrations, "rank": rank, "transport": transport, "layers": layers,
     }
     scale = {"dq": rdq.float().abs().max().item(), "dk": rdk.float().abs().max().item(),
              "dv": rdv.float().abs().max().item()}
