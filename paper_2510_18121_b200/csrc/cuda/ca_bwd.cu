@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
       const float lse2 = valid ? -p.lse2[int64_t(un.head0) * p.pitch + row] : 0.f;
       const float dd = valid ? -p.delta[int64_t(un.head0) * p.pitch + row] : 0.f;
       const int pos = valid ? shift + qi : -1;  // invalid rows see nothing
+      const bool all_rows = un.tile * kTile + kTile <= tk.n_q;
       for (int j = 0; j < un.n_kv; ++j) {
         mbar_wait_warp(&bars->s_full, s_ph);
         s_ph ^= 1;
@@ -710,6 +711,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         tc_fence_before();
         mbar_arrive(&bars->p_read);
         const int lim = pos - (j * kTile + c0);  // last visible column
+        // mask-free (CTA-uniform) when every row of the tile is a query and
+        // its first row already sees this warpgroup's last column
+        const bool full = all_rows && shift + un.tile * kTile - (j * kTile + c0) >= 63;
         const uint64_t sc2 = f2(p.scale_log2, p.scale_log2), nl2 = f2(-lse2, -lse2);
 #pragma unroll
         for (int k = 0; k < 64; k += 2) {
@@ -721,8 +725,12 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
             a = ex2(a);
             b = ex2(b);
           }
-          x[k] = k <= lim ? a : 0.f;
-          x[k + 1] = k + 1 <= lim ? b : 0.f;
+          x[k] = a;
+          x[k + 1] = b;
+        }
+        if (!full) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) x[k] = k <= lim ? x[k] : 0.f;
         }
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
