@@ -133,8 +133,9 @@ def run(args, metric, load_peaks, ClockSampler):
         torch.cuda.synchronize()
         tr = layer.ce.trace
         layer.ce.trace = None
-        t0 = [x for x in tr if x[0] == "F"][0][3]
-        trace = sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
+        fw = [x for x in tr if x[0] == "F"]
+        t0 = fw[0][3] if fw else None
+        trace = None if t0 is None else sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
                          round(b.elapsed_time(c), 2)) for (k, l, h, a, b, c) in tr], key=lambda r: r[3])
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_, hdo_)) * world
     d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv)) * world

@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -21,6 +22,7 @@
 
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
+#include "sm100.cuh"
 
 namespace {
 
@@ -225,6 +227,82 @@ __global__ void __launch_bounds__(512) copy_spans_kernel(const cad_span* spans, 
   }
 }
 
+
+// TMA bulk variant (one CTA per SM left free by the CA kernels): thread 0
+// streams 16-byte aligned spans in batches of kBulkBufs 32 KB chunks,
+// global -> shared (mbarrier complete_tx) -> global (dst may be a peer
+// mapping: the write crosses NVLink). Spans that are not 16-byte aligned
+// (LSE columns) are copied by all threads with 4-byte words.
+constexpr int kBulkChunk = 32768, kBulkBufs = 6;
+constexpr int kBulkSmem = kBulkChunk * kBulkBufs;
+
+__global__ void __launch_bounds__(256) copy_spans_bulk_kernel(const cad_span* spans, int64_t n) {
+  extern __shared__ __align__(128) uint8_t cbuf[];
+  __shared__ uint64_t bar[kBulkBufs];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBulkBufs; ++i) mbar_init(&bar[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // unaligned spans: word copies, chunks dealt round-robin over the CTAs
+  int64_t base = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const cad_span sp = spans[i];
+    const bool aligned = ((reinterpret_cast<uintptr_t>(sp.src) | reinterpret_cast<uintptr_t>(sp.dst) |
+                           static_cast<uint64_t>(sp.bytes)) & 15) == 0;
+    const int64_t chunks = (sp.bytes + kBulkChunk - 1) / kBulkChunk;
+    if (!aligned) {
+      for (int64_t c = (blockIdx.x - base % gridDim.x + gridDim.x) % gridDim.x; c < chunks; c += gridDim.x) {
+        const int64_t off = c * kBulkChunk, len = min(int64_t(kBulkChunk), sp.bytes - off);
+        const int* s1 = reinterpret_cast<const int*>(static_cast<const char*>(sp.src) + off);
+        int* d1 = reinterpret_cast<int*>(static_cast<char*>(sp.dst) + off);
+        for (int64_t k = threadIdx.x; k < len / 4; k += blockDim.x) d1[k] = s1[k];
+      }
+    }
+    base += chunks;
+  }
+  if (threadIdx.x != 0) return;
+  const uint32_t sb = smem_u32(cbuf);
+  uint32_t phase = 0;  // all slots complete one phase per batch
+  int nb = 0;          // loads in the current batch
+  const char* bdst[kBulkBufs];
+  int blen[kBulkBufs];
+  auto flush = [&]() {
+    for (int s = 0; s < nb; ++s) {
+      mbar_wait(&bar[s], phase);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   :: "l"(bdst[s]), "r"(sb + s * kBulkChunk), "r"(blen[s]) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slots reusable
+    phase ^= 1;
+    nb = 0;
+  };
+  base = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const cad_span sp = spans[i];
+    const bool aligned = ((reinterpret_cast<uintptr_t>(sp.src) | reinterpret_cast<uintptr_t>(sp.dst) |
+                           static_cast<uint64_t>(sp.bytes)) & 15) == 0;
+    const int64_t chunks = (sp.bytes + kBulkChunk - 1) / kBulkChunk;
+    if (aligned) {
+      for (int64_t c = (blockIdx.x - base % gridDim.x + gridDim.x) % gridDim.x; c < chunks; c += gridDim.x) {
+        const int64_t off = c * kBulkChunk;
+        const int len = static_cast<int>(min(int64_t(kBulkChunk), sp.bytes - off));
+        mbar_expect_tx(&bar[nb], len);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            :: "r"(sb + nb * kBulkChunk), "l"(static_cast<const char*>(sp.src) + off), "r"(len),
+               "r"(smem_u32(&bar[nb])) : "memory");
+        bdst[nb] = static_cast<const char*>(sp.dst) + off;
+        blen[nb] = len;
+        if (++nb == kBulkBufs) flush();
+      }
+    }
+    base += chunks;
+  }
+  if (nb) flush();
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
+}
 }  // namespace cad_dev
 
 extern "C" {
@@ -395,7 +473,20 @@ int cad_copy_spans(const cad_span* spans, int64_t n, int32_t n_ctas, void* strea
   return cad::guarded([&] {
     if (n == 0) return;
     if (!spans || n_ctas < 1) throw cad::DomainError("bad argument");
-    cad_dev::copy_spans_kernel<<<n_ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(spans, n);
+    static const bool simt = std::getenv("CAD_COPY_SIMT") != nullptr;
+    if (simt) {
+      cad_dev::copy_spans_kernel<<<n_ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(spans, n);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        cad_dev::cuda_check(cudaFuncSetAttribute(cad_dev::copy_spans_bulk_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, cad_dev::kBulkSmem),
+                            "cudaFuncSetAttribute(copy_spans_bulk)");
+        attr = true;
+      }
+      cad_dev::copy_spans_bulk_kernel<<<n_ctas, 256, cad_dev::kBulkSmem, static_cast<cudaStream_t>(stream)>>>(
+          spans, n);
+    }
     cad_dev::cuda_check(cudaGetLastError(), "copy_spans launch");
   });
 }
