@@ -129,7 +129,7 @@ def run(args, metric, load_peaks, ClockSampler):
     if os.environ.get("CAD_TRACE") and layer.ce is not None:
         # per-kernel flag waits on the compute stream in one ping-pong step
         layer.ce.trace = []
-        step()
+        step(os.environ.get("CAD_TRACE_MODE", "pingpong"))
         torch.cuda.synchronize()
         tr = layer.ce.trace
         layer.ce.trace = None

@@ -21,6 +21,7 @@ provides device memory, streams and events.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence
 
@@ -377,6 +378,7 @@ class DistCALayer:
 # without host synchronisation.
 
 F_QKV, F_DO, F_O, F_G, F_DONE = 0, 1, 2, 3, 4  # flag kinds (x2 halves, F_DONE uses half 0)
+_DEBUG_COPY = bool(os.environ.get("CAD_DEBUG_COPY"))  # per-copy timing prints (rank 0)
 
 
 def _runs(src: np.ndarray, dst: np.ndarray) -> np.ndarray:
@@ -484,6 +486,8 @@ class CETransport:
         self.launches = 0
         self.move = True
         self.trace = None  # list of (kind, layer, half, ev_before_wait, ev_after_wait, ev_done) when tracing
+        self.local_stream = None  # set per step: the compute stream (own rows are copied there)
+        self.local_on_comp = os.environ.get("CAD_LOCAL_ON_COMP", "1") != "0"
         # 'ce': copy-engine memcpys; 'sm': one copy kernel per transfer on
         # copy_ctas SMs left free by the CA kernels (the CA kernels' L2
         # traffic starves the copy engines)
@@ -522,6 +526,8 @@ class CETransport:
             if spans is None:
                 rows = []
                 for p in range(self.W):
+                    if p == self.me and self.local_stream is not None:
+                        continue  # local rows: copy engine on the compute stream (below)
                     rl = self.runs[(h, x, p)]
                     dst = self.peer[p][dst_name]
                     for r in rl.arr_np:
@@ -531,14 +537,33 @@ class CETransport:
                 spans = (spans, len(rows))
                 self._spans[key] = spans
             if spans[1]:
+                if _DEBUG_COPY and self.me == 0:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
                 check(lib().cad_copy_spans(spans[0].data_ptr(), spans[1], self.copy_ctas, stream.cuda_stream))
+                if _DEBUG_COPY and self.me == 0:
+                    e1.record(stream)
+                    e1.synchronize()
+                    sp = spans[0].cpu()
+                    print(f"copy {key[:2]} {key[-2:]} spans={spans[1]} bytes={int(sp[:, 2].sum())} "
+                          f"max_span={int(sp[:, 2].max())} ms={e0.elapsed_time(e1):.3f}", flush=True)
                 self.launches += 1
+            if self.local_stream is not None:
+                rl = self.runs[(h, x, self.me)]
+                if rl.n:
+                    check(lib().cad_copy_runs(rl.arr, rl.n, src_ptr, self.peer[self.me][dst_name], row_bytes,
+                                              self.local_stream.cuda_stream))
             return
         for p in range(self.W):
             rl = self.runs[(h, x, p)]
             if rl.n:
+                # this rank's own rows move between its home and server buffers on
+                # the compute stream, between kernels: a local copy overlapping a
+                # CA kernel runs 10-30x slower (the kernels' L2 traffic starves the
+                # copy engines) and would delay the remote pushes queued behind it
+                st = self.local_stream if (p == self.me and self.local_stream is not None) else stream
                 check(lib().cad_copy_runs(rl.arr, rl.n, src_ptr, self.peer[p][dst_name], row_bytes,
-                                          stream.cuda_stream))
+                                          st.cuda_stream))
 
     def _push(self, h, x, src, dst_name, row_bytes, stream):
         if not self.move:
@@ -556,6 +581,8 @@ class CETransport:
                 rows = []
                 sr = src_lse.shape[1]
                 for p in range(self.W):
+                    if p == self.me and self.local_stream is not None:
+                        continue
                     rl = self.runs[(h, XFER_O_RET, p)]
                     dr = self.plans[p].home_rows
                     for r in rl.arr_np:
@@ -565,15 +592,27 @@ class CETransport:
                 spans = (torch.tensor(rows if rows else [(0, 0, 0)], dtype=torch.int64).to(L.dev), len(rows))
                 self._spans[key] = spans
             if spans[1]:
+                if _DEBUG_COPY and self.me == 0:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
                 check(lib().cad_copy_spans(spans[0].data_ptr(), spans[1], self.copy_ctas, stream.cuda_stream))
+                if _DEBUG_COPY and self.me == 0:
+                    e1.record(stream)
+                    e1.synchronize()
+                    sp = spans[0].cpu()
+                    print(f"copy {key[:2]} {key[-2:]} spans={spans[1]} bytes={int(sp[:, 2].sum())} "
+                          f"max_span={int(sp[:, 2].max())} ms={e0.elapsed_time(e1):.3f}", flush=True)
                 self.launches += 1
-            return
-        for p in range(self.W):
+            peers = [self.me] if self.local_stream is not None else []
+        else:
+            peers = range(self.W)
+        for p in peers:
             rl = self.runs[(h, XFER_O_RET, p)]
             if rl.n:
                 dst_rows = self.plans[p].home_rows
+                st = self.local_stream if (p == self.me and self.local_stream is not None) else stream
                 check(lib().cad_copy_runs_cols(rl.arr, rl.n, src_lse.data_ptr(), src_lse.shape[1],
-                                               self.peer[p]["lse"], dst_rows, L.hq, stream.cuda_stream))
+                                               self.peer[p]["lse"], dst_rows, L.hq, st.cuda_stream))
 
     def step(self, q, k, v, do, dk_acc, dv_acc, compute: bool = True, move: bool = True):
         """One step = self.layers CA layers, forward then backward.
@@ -595,6 +634,7 @@ class CETransport:
         self.move = move
         comp = torch.cuda.current_stream(L.dev)
         comm = L.comm_stream
+        self.local_stream = comp if self.local_on_comp else None
         self.gen += 1
         g = self.gen
         start = torch.cuda.Event()
@@ -667,6 +707,7 @@ class CETransport:
         self.move = move
         comp = torch.cuda.current_stream(L.dev)
         comm = L.comm_stream
+        self.local_stream = comp if self.local_on_comp else None
         # flag values of this step, increasing in issue order (waits are >=):
         # forward layer l -> g0 + 1 + l, backward layer l -> g0 + 2 NL - l,
         # F_DONE -> g0 + 2 NL
