@@ -6,7 +6,7 @@ placed sequentially; CA-tasks sharded by the bit-exact scheduler; per layer
 the Q/KV dispatch, CA fwd, O/LSE return, dO dispatch, CA bwd, dQ and dK/dV
 return run with ping/pong halves (dispatch.py) over copy-engine pushes
 (CUDA IPC, default; CAD_TRANSPORT=nccl for NCCL all-to-allv). A step is
-CAD_LAYERS (default 1) stacked CA layers, forward then backward, with the
+CAD_LAYERS (default 4) stacked CA layers, forward then backward, with the
 identity between layers, so transfers of one layer overlap the neighbouring
 layer's CA compute. Scaling is weak (fixed tokens per GPU). Times are CUDA
 events on the compute stream, max over ranks.
@@ -79,7 +79,7 @@ def run(args, metric, load_peaks, ClockSampler):
     comp = torch.cuda.current_stream(dev)
     # stacked CA layers per step (copy-engine transport): the dispatch of
     # layer l+1 and the return of layer l overlap the other half's CA
-    layers = int(os.environ.get("CAD_LAYERS", "1")) if transport == "ce" else 1
+    layers = int(os.environ.get("CAD_LAYERS", "4")) if transport == "ce" else 1
     if transport == "ce":
         layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq,
                                layers=layers, copy_mode=copy_mode, copy_ctas=copy_ctas)
