@@ -47,7 +47,7 @@ void run(const char* name, int threads) {
 }
 
 int main() {
-  for (int t : {256, 512, 1024}) {
+  for (int t : {128, 256, 512}) {
     run<0>("ex2", t); run<1>("cvt.bf16x2", t); run<2>("max", t); run<3>("fma", t); run<4>("fma.f32x2", t);
     run<5>("max3", t);
   }
