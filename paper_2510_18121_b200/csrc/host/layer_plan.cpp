@@ -15,6 +15,13 @@
 //          SURVEY.md 8f next #1; the reference charges the full prefix per
 //          remote task and nothing for home-served straddling documents,
 //          P/src/scheduler.cpp:342-345).
+// head_tail items (per-document CP layouts, P/include/cadsim/types.hpp:101-111)
+// are served as two CA-tasks sharing the document's KV group: the head
+// [q_begin, q_end) over keys [0, q_end) and the tail
+// [M - q_end, M - q_begin) over keys [0, M - q_begin), M = ht_mirror (the
+// reference's two sub-calls, P/src/sim.cpp:22-30, P/src/cost.cpp:40-43). A
+// head_tail home item holds its head rows, then its tail rows (the chunk
+// segment order of P/src/experiment.cpp:120-130).
 // Exchanges (per half, row granularity, every rank including itself):
 //   QD  Q (and dO in backward) home -> server     KVD K/V home -> server
 //   OR  O/LSE (and dQ in backward) server -> home  KVR dK/dV server -> owner
@@ -133,6 +140,10 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
       i64& r = rows_of[static_cast<size_t>(it.home_device)];
       owners[it.doc].push_back({it.q_begin, it.q_end, it.home_device, r});
       r += it.q_end - it.q_begin;
+      if (it.layout == CAD_LAYOUT_HEAD_TAIL) {
+        owners[it.doc].push_back({it.ht_mirror - it.q_end, it.ht_mirror - it.q_begin, it.home_device, r});
+        r += it.q_end - it.q_begin;
+      }
     }
     for (auto& kv : owners)
       std::sort(kv.second.begin(), kv.second.end(), [](const Seg& a, const Seg& b) { return a.begin < b.begin; });
@@ -152,14 +163,14 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
         for (const cad::Served& sv : devs[static_cast<size_t>(s)].served) {
           if (sv.half != h) continue;
           const cad::Item& it = P.tasks[static_cast<size_t>(sv.task)].item;
-          if (it.layout != cad::Layout::contiguous)
-            throw cad::DomainError("head_tail CA-tasks are not supported by the dispatcher");
+          const i64 need = it.layout == cad::Layout::head_tail ? std::max(it.kv_extent, it.ht_mirror - it.q_begin)
+                                                               : it.kv_extent;
           auto g = group.find(it.doc);
           if (g == group.end()) {
-            group[it.doc] = {0, it.kv_extent};
+            group[it.doc] = {0, need};
             doc_order.push_back(it.doc);
           } else {
-            g->second.second = std::max(g->second.second, it.kv_extent);
+            g->second.second = std::max(g->second.second, need);
           }
         }
         i64 kv_off = 0;
@@ -172,21 +183,29 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
           if (sv.half != h) continue;
           const cad::Task& t = P.tasks[static_cast<size_t>(sv.task)];
           const cad::Item& it = t.item;
-          cad_ca_task ct;
-          ct.q_off = H.q_rows;
-          ct.n_q = it.n_q();
-          ct.kv_off = group[it.doc].first;
-          ct.kv_len = it.kv_extent;
-          H.tasks.push_back(ct);
-          H.task_index.push_back(sv.task);
-          // Q rows come from the task's home device
+          // (query begin, end) of the CA-tasks of this item: its head, and
+          // for head_tail its mirrored tail; each sees keys [0, end)
+          std::pair<i64, i64> parts[2] = {{it.q_begin, it.q_end}, {0, 0}};
+          int n_parts = 1;
+          if (it.layout == cad::Layout::head_tail) parts[n_parts++] = {it.ht_mirror - it.q_end, it.ht_mirror - it.q_begin};
           const auto& segs = owners.at(it.doc);
-          for (i64 pos = it.q_begin; pos < it.q_end; ++pos) {
-            const Seg& o = owner_of(segs, pos);
-            if (o.device != it.home) throw cad::DomainError("task rows not on its home device");
-            qd.add(o.device, s, o.home_row + (pos - o.begin), H.q_rows + (pos - it.q_begin));
+          for (int k = 0; k < n_parts; ++k) {
+            const i64 qb = parts[k].first, qe = parts[k].second;
+            cad_ca_task ct;
+            ct.q_off = H.q_rows;
+            ct.n_q = qe - qb;
+            ct.kv_off = group[it.doc].first;
+            ct.kv_len = qe;
+            H.tasks.push_back(ct);
+            H.task_index.push_back(sv.task);
+            // Q rows come from the task's home device
+            for (i64 pos = qb; pos < qe; ++pos) {
+              const Seg& o = owner_of(segs, pos);
+              if (o.device != it.home) throw cad::DomainError("task rows not on its home device");
+              qd.add(o.device, s, o.home_row + (pos - o.begin), H.q_rows + (pos - qb));
+            }
+            H.q_rows += qe - qb;
           }
-          H.q_rows += it.n_q();
         }
         for (i64 d : doc_order) {
           const auto& segs = owners.at(d);

@@ -73,11 +73,16 @@ class LayerPlan:
     """Schedule + per-rank row movement of one layer (host side, no GPU)."""
 
     def __init__(self, lengths: Sequence[int], world: int, rank: int, shape: CF.Shape,
-                 cfg: Optional[S.SchedulerConfig] = None, tokens_per_device: Optional[int] = None):
+                 cfg: Optional[S.SchedulerConfig] = None, tokens_per_device: Optional[int] = None,
+                 items: Optional[Sequence[S.Item]] = None):
+        """Home items from place_sequential(lengths) (DistCA's chunks), or the
+        given `items` (e.g. head_tail per-document CP shards; a head_tail
+        item's home rows are its head rows, then its tail rows)."""
         total = sum(lengths)
         self.world, self.rank, self.shape = world, rank, shape
         self.tokens_per_device = tokens_per_device or total // world
-        self.home_items = S.place_sequential(lengths, world, self.tokens_per_device)
+        self.home_items = list(items) if items is not None else S.place_sequential(lengths, world,
+                                                                                   self.tokens_per_device)
         self.cfg = cfg or CF.sched_config(shape)
         ph = S.PlanHandle(self.home_items, world, self.cfg)
         self.plan = ph.plan

@@ -6,6 +6,7 @@ import numpy as np
 
 import oracle
 from paper_2510_18121_b200 import dispatch as D
+from paper_2510_18121_b200 import scheduler as S
 
 
 def split(counts, arr):
@@ -40,15 +41,21 @@ def home_arrays(plans, lengths, per_doc):
     homes = []
     for r in range(W):
         items = [it for it in plans[0].home_items if it.home_device == r]
-        homes.append(np.concatenate([per_doc[it.doc][it.q_begin:it.q_end] for it in items]))
+        parts = []
+        for it in items:
+            parts.append(per_doc[it.doc][it.q_begin:it.q_end])
+            if it.layout == S.HEAD_TAIL:  # tail rows follow the head rows
+                parts.append(per_doc[it.doc][it.ht_mirror - it.q_end:it.ht_mirror - it.q_begin])
+        homes.append(np.concatenate(parts))
     return homes
 
 
-def run_layer(lengths, world, shape, seed=0):
+def run_layer(lengths, world, shape, seed=0, items=None):
     """Returns (home outputs of the distributed run, whole-batch reference),
-    both in home layout per rank: dicts of o, lse, dq, dk, dv."""
+    both in home layout per rank: dicts of o, lse, dq, dk, dv. `items`:
+    explicit home items (default: place_sequential of the lengths)."""
     rng = np.random.default_rng(seed)
-    plans = [D.LayerPlan(lengths, world, r, shape) for r in range(world)]
+    plans = [D.LayerPlan(lengths, world, r, shape, items=items) for r in range(world)]
     hq, hkv, d = shape.h_q, shape.h_kv, shape.head_dim
     per = {n: [rng.standard_normal((l, h, d), dtype=np.float32) for l in lengths]
            for n, h in (("q", hq), ("k", hkv), ("v", hkv), ("do", hq))}

@@ -52,3 +52,44 @@ def test_remote_bytes_residency_aware():
             for peer in range(3):
                 seg = np.split(x.send_idx, np.cumsum(x.send_counts)[:-1])[peer]
                 assert len(np.unique(seg)) == len(seg)
+
+
+def head_tail_partition(doc, begin, end, cp, first_rank):
+    """Restates P/src/baselines.cpp:86-133 (per-document CP shards): rank k
+    holds the mirror-symmetric pair [p_k, p_k+1) + [M-p_k+1, M-p_k); an odd
+    middle slice goes to the last rank as a contiguous shard."""
+    from paper_2510_18121_b200 import scheduler as S
+    span, mirror = end - begin, begin + end
+    p = [0] * (2 * cp + 1)
+    for k in range(cp + 1):
+        p[k] = begin + (span * k) // (2 * cp)
+    for k in range(cp + 1, 2 * cp + 1):
+        p[k] = mirror - p[2 * cp - k]
+    items = []
+    for k in range(cp):
+        lo, hi = p[k], p[k + 1]
+        if hi <= lo:
+            continue
+        items.append(S.Item(doc, lo, hi, hi, mirror, first_rank + k, S.HEAD_TAIL))
+    mid_lo, mid_hi = p[cp], mirror - p[cp]
+    if mid_hi > mid_lo:
+        items.append(S.Item(doc, mid_lo, mid_hi, mid_hi, 0, first_rank + cp - 1, S.CONTIGUOUS))
+    return items
+
+
+@pytest.mark.parametrize("world,cp,lengths", [
+    (2, 2, [700, 61, 120, 401, 256, 512]),    # every document split head/tail over both ranks
+    (4, 2, [900, 33, 250, 300, 128, 517]),    # two CP groups; the scheduler migrates shards
+])
+def test_head_tail_items_match_whole_batch(world, cp, lengths):
+    """head_tail items: each is served as two CA-tasks
+    (head and mirrored tail) sharing the document's KV group."""
+    items = []
+    for d, l in enumerate(lengths):
+        items += head_tail_partition(d, 0, l, cp, (d % (world // cp)) * cp)
+    out, ref, plans = run_layer(lengths, world, SHAPE, seed=7, items=items)
+    assert any(t.n_q > 0 for hp in plans[0].halves for t in hp.tasks)
+    for r in range(world):
+        for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
+            err = np.abs(out[name][r] - ref[name][r]).max()
+            assert err < tol, (r, name, err)
