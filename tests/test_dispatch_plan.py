@@ -93,3 +93,31 @@ def test_head_tail_items_match_whole_batch(world, cp, lengths):
         for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
             err = np.abs(out[name][r] - ref[name][r]).max()
             assert err < tol, (r, name, err)
+
+
+def test_pp_tick_plan_executes():
+    """A pipeline-parallel tick: schedule_pp_tick
+    re-homes every stage's items to the stage index and schedules the pool
+    (P/src/scheduler.cpp:359-373); the dispatcher executes that plan like any
+    other layer plan."""
+    from paper_2510_18121_b200 import configs as CF2
+    from paper_2510_18121_b200 import scheduler as S
+    stages = [[500, 301], [200, 700, 99]]  # document lengths per PP stage
+    lengths, per_stage, doc = [], [], 0
+    for st, ls in enumerate(stages):
+        its = []
+        for l in ls:
+            its.append(S.Item(doc, 0, l, l, 0, 0, S.CONTIGUOUS))
+            lengths.append(l)
+            doc += 1
+        per_stage.append(its)
+    cfg = CF2.sched_config(SHAPE)
+    tick = S.schedule_pp_tick(per_stage, 2, cfg)
+    rehomed = [S.Item(it.doc, it.q_begin, it.q_end, it.kv_extent, it.ht_mirror, st, it.layout)
+               for st, its in enumerate(per_stage) for it in its]
+    out, ref, plans = run_layer(lengths, 2, SHAPE, seed=11, items=rehomed)
+    assert plans[0].plan.text == tick.text
+    for r in range(2):
+        for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
+            err = np.abs(out[name][r] - ref[name][r]).max()
+            assert err < tol, (r, name, err)
