@@ -229,18 +229,48 @@ def single_gpu(args):
     h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, hdo))
     d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv))
 
-    def e2e_step():
-        q.copy_(hq, non_blocking=True)
-        k.copy_(hk, non_blocking=True)
-        v.copy_(hv, non_blocking=True)
-        do.copy_(hdo, non_blocking=True)
-        step()
-        hdq.copy_(dq, non_blocking=True)
-        hdk.copy_(dk, non_blocking=True)
-        hdv.copy_(dv, non_blocking=True)
+    # Double-buffered: step j's inputs go host -> device on a copy stream while
+    # step j-1 computes, and step j's gradients come back while step j+1
+    # computes; every step still moves its own inputs and results.
+    sets = [(q, k, v, do, o, lse, dq, dk, dv),
+            tuple(torch.empty_like(t) for t in (q, k, v, do, o, lse, dq, dk, dv))]
+    copy = torch.cuda.Stream(device=dev)
 
-    e2e_step()
-    e2e_ms = time_region(e2e_step, max(2, min(args.steps, 5)), stream)
+    def e2e_run(n):
+        ev = torch.cuda.Event
+        h2d_done, comp_done = [None, None], [None, None]
+        st, en = ev(enable_timing=True), ev(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record(copy)
+        for j in range(n + 1):
+            if j < n:  # inputs of step j
+                b = sets[j % 2]
+                if comp_done[j % 2] is not None:
+                    copy.wait_event(comp_done[j % 2])  # step j-2 done with this set
+                with torch.cuda.stream(copy):
+                    for dst, src in zip(b[:4], (hq, hk, hv, hdo)):
+                        dst.copy_(src, non_blocking=True)
+                h2d_done[j % 2] = ev()
+                h2d_done[j % 2].record(copy)
+            if j >= 1:  # results of step j-1
+                with torch.cuda.stream(copy):
+                    copy.wait_event(comp_done[(j - 1) % 2])
+                    b = sets[(j - 1) % 2]
+                    for dst, src in zip((hdq, hdk, hdv), b[6:]):
+                        dst.copy_(src, non_blocking=True)
+            if j < n:  # compute step j
+                b = sets[j % 2]
+                stream.wait_event(h2d_done[j % 2])
+                plan.forward(b[0], b[1], b[2], b[4], b[5])
+                plan.backward(b[0], b[1], b[2], b[4], b[5], b[3], b[6], b[7], b[8], ws)
+                comp_done[j % 2] = ev()
+                comp_done[j % 2].record(stream)
+        en.record(copy)
+        torch.cuda.synchronize()
+        return st.elapsed_time(en) / n
+
+    e2e_run(2)
+    e2e_ms = e2e_run(max(3, min(args.steps, 6)))
 
     peak, peak_sus, peak_kind = load_peaks()
     value = flops["total"] / ms / 1e9
