@@ -142,20 +142,38 @@ namespace kv {
 #endif
 // one bit per group of 4 q columns: 1 = polynomial exp2 on the FMA pipe
 constexpr uint32_t kDkdvEmuMask = CAD_DKDV_EMU_MASK;
-constexpr int kStages = 2;
+// Q tiles are staged 3 deep and dO tiles 2 deep: S^T(i+1) needs Q(i+1)
+// right after dV(i), while Q(i) still feeds dK(i) and the slot of Q(i-1)
+// only frees after dK(i-1) -- with 2 stages the MMA warp waited ~280 cycles
+// per iteration for Q(i+1) to land (clock64 trace, scripts/timeline_dkdv.py).
+constexpr int kQStages = 3, kDOStages = 2;
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
-constexpr uint32_t kQOff = 2 * kTileBytes;                  // kStages x 32 KB
-constexpr uint32_t kDOOff = kQOff + kStages * kTileBytes;   // kStages x 32 KB
-constexpr uint32_t kRowOff = kDOOff + kStages * kTileBytes; // [stage][-LSE 128 | -D 128] fp32
-constexpr uint32_t kBarOff = kRowOff + kStages * 1024;
-constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
+constexpr uint32_t kQOff = 2 * kTileBytes;                    // kQStages x 32 KB
+constexpr uint32_t kDOOff = kQOff + kQStages * kTileBytes;    // kDOStages x 32 KB
+constexpr uint32_t kLseOff = kDOOff + kDOStages * kTileBytes; // [q stage][128] -LSE*log2e fp32
+constexpr uint32_t kDOff = kLseOff + kQStages * 512;          // [dO stage][128] -D fp32
+constexpr uint32_t kBarOff = kDOff + kDOStages * 512;
+// Dynamic shared memory starts 1024-aligned (no static shared memory in this
+// kernel; checked at run time), so the budget carries no alignment slack.
+constexpr uint32_t kSmemBytes = kBarOff + 256;
+static_assert(kSmemBytes <= 232448, "dK/dV shared memory");
 
 struct Bars {
   uint64_t kv_full, kv_empty;
-  uint64_t in_full[kStages], in_empty[kStages];
+  uint64_t q_full[kQStages], q_empty[kQStages], do_full[kDOStages], do_empty[kDOStages];
   uint64_t s_full, dp_full, p_half, p_full, ds_half, ds_full, acc_full, acc_free;
   uint32_t tmem_base;
+};
+static_assert(sizeof(Bars) <= 256, "dK/dV barriers");
+
+// Slot index + phase of a ring of N stages.
+template <int N>
+struct KRing {
+  uint32_t i = 0, ph = 0;
+  __device__ void next() {
+    if (++i == N) { i = 0; ph ^= 1; }
+  }
 };
 
 struct Params {
@@ -196,12 +214,13 @@ struct Cursor {
 };
 
 __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_constant__ Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
-  float* rows = reinterpret_cast<float*>(smem + kRowOff);
+  float* lse_rows = reinterpret_cast<float*>(smem + kLseOff);
+  float* d_rows = reinterpret_cast<float*>(smem + kDOff);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t warp = warp_id(), lane = lane_id();
+  if (sbase & 1023) __trap();  // SW128 tiles need 1024-byte alignment
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&p.tm_q);
@@ -210,9 +229,13 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
     tma_prefetch(&p.tm_do);
     mbar_init(&bars->kv_full, 1);
     mbar_init(&bars->kv_empty, 1);
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&bars->in_full[i], 33);
-      mbar_init(&bars->in_empty[i], 1);
+    for (int i = 0; i < kQStages; ++i) {
+      mbar_init(&bars->q_full[i], 33);
+      mbar_init(&bars->q_empty[i], 1);
+    }
+    for (int i = 0; i < kDOStages; ++i) {
+      mbar_init(&bars->do_full[i], 33);
+      mbar_init(&bars->do_empty[i], 1);
     }
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
@@ -237,9 +260,12 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       // ---------------------------------------------------------- producer
       // Lane 0 issues the TMA tile loads; the whole warp copies the tile's
       // 128 -LSE and 128 -D values (arbitrary, unaligned row offsets, so
-      // cp.async rather than TMA); each lane's async arrive lands on in_full
-      // when its copies have (count 1 + 32).
-      uint32_t kv_it = 0, st = 0, ph = 0;
+      // cp.async rather than TMA); each lane's async arrives land on q_full
+      // (-LSE, with Q) and do_full (-D, with dO) when its copies have (count
+      // 1 + 32 each).
+      uint32_t kv_it = 0;
+      KRing<kQStages> qr;
+      KRing<kDOStages> dr;
       for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
         const int u = sched_unit(p.sched, gridDim.x, ui);
         const KvUnit un = p.units[u];
@@ -259,34 +285,44 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           const DevTask tk = p.tasks[p.segs[c.seg].task];
           const int head = un.hk * p.group + c.g;
           const int qrow = tk.q_off + c.qt * kTile;
-          mbar_wait(&bars->in_empty[st], ph ^ 1);
-          if (lane == 0) {
-            mbar_expect_tx(&bars->in_full[st], 2 * kTileBytes);
-            uint8_t* q = smem + kQOff + st * kTileBytes;
-            uint8_t* d = smem + kDOOff + st * kTileBytes;
-            tma_load_3d(&p.tm_q, &bars->in_full[st], q, 0, qrow, head);
-            tma_load_3d(&p.tm_q, &bars->in_full[st], q + kTileBytes / 2, 64, qrow, head);
-            tma_load_3d(&p.tm_do, &bars->in_full[st], d, 0, qrow, head);
-            tma_load_3d(&p.tm_do, &bars->in_full[st], d + kTileBytes / 2, 64, qrow, head);
-          }
-          float* dst = rows + st * 256;
           const float* nl = p.nlse2 + int64_t(head) * p.pitch;
           const float* nd = p.ndelta + int64_t(head) * p.pitch;
+          // rows past the buffer only feed masked columns: clamp the source
+          mbar_wait(&bars->q_empty[qr.i], qr.ph ^ 1);
+          if (lane == 0) {
+            mbar_expect_tx(&bars->q_full[qr.i], kTileBytes);
+            uint8_t* q = smem + kQOff + qr.i * kTileBytes;
+            tma_load_3d(&p.tm_q, &bars->q_full[qr.i], q, 0, qrow, head);
+            tma_load_3d(&p.tm_q, &bars->q_full[qr.i], q + kTileBytes / 2, 64, qrow, head);
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int col = lane + 32 * k;
-            // rows past the buffer only feed masked columns: clamp the source
-            const int64_t rrow = min(int64_t(qrow) + col, p.pitch - 1);
-            cp_async4(dst + col, nl + rrow);
-            cp_async4(dst + 128 + col, nd + rrow);
+            cp_async4(lse_rows + qr.i * 128 + col, nl + min(int64_t(qrow) + col, p.pitch - 1));
           }
-          cp_async_arrive(&bars->in_full[st]);
-          if (++st == kStages) { st = 0; ph ^= 1; }
+          cp_async_arrive(&bars->q_full[qr.i]);
+          qr.next();
+          mbar_wait(&bars->do_empty[dr.i], dr.ph ^ 1);
+          if (lane == 0) {
+            mbar_expect_tx(&bars->do_full[dr.i], kTileBytes);
+            uint8_t* d = smem + kDOOff + dr.i * kTileBytes;
+            tma_load_3d(&p.tm_do, &bars->do_full[dr.i], d, 0, qrow, head);
+            tma_load_3d(&p.tm_do, &bars->do_full[dr.i], d + kTileBytes / 2, 64, qrow, head);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int col = lane + 32 * k;
+            cp_async4(d_rows + dr.i * 128 + col, nd + min(int64_t(qrow) + col, p.pitch - 1));
+          }
+          cp_async_arrive(&bars->do_full[dr.i]);
+          dr.next();
         }
       }
     } else if (warp == 9) {
       // ---------------------------------------------------------- MMA
-      uint32_t kv_it = 0, st = 0, ph = 0, acc_it = 0, p_ph = 0, ds_ph = 0;
+      uint32_t kv_it = 0, acc_it = 0, p_ph = 0, ds_ph = 0;
+      KRing<kQStages> qr;
+      KRing<kDOStages> dr;
       const uint32_t sK = sbase + kKOff, sV = sbase + kVOff;
       for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
         const int u = sched_unit(p.sched, gridDim.x, ui);
@@ -294,15 +330,19 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         const int n = un.n_iter;
         mbar_wait(&bars->kv_full, kv_it & 1);
         ++kv_it;
-        mbar_wait(&bars->in_full[st], ph);
+        mbar_wait(&bars->q_full[qr.i], qr.ph);
         tc_fence_after();
-        uint32_t sQ = sbase + kQOff + st * kTileBytes, sDO = sbase + kDOOff + st * kTileBytes;
+        uint32_t sQ = sbase + kQOff + qr.i * kTileBytes, sDO = sbase + kDOOff + dr.i * kTileBytes;
         issue_qk(tS, sK, sQ);
         mma_commit(&bars->s_full);
+        mbar_wait(&bars->do_full[dr.i], dr.ph);
+        tc_fence_after();
         issue_qk(tDP, sV, sDO);
         mma_commit(&bars->dp_full);
         for (int i = 0; i < n; ++i) {
-          const uint32_t cur = st;
+          const uint32_t qcur = qr.i, dcur = dr.i;
+          qr.next();
+          dr.next();
           // dV += P^T dO, in two K-halves (q columns [0,64) and [64,128)) as
           // the warpgroups release them
           mbar_wait(&bars->p_half, p_ph);
@@ -316,13 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           p_ph ^= 1;
           tc_fence_after();
           issue_pv_half(tDV, tS + 80, sDO, 1, true);
-          uint32_t nQ = 0, nDO = 0;
+          const uint32_t nQ = sbase + kQOff + qr.i * kTileBytes, nDO = sbase + kDOOff + dr.i * kTileBytes;
           if (i + 1 < n) {
-            if (++st == kStages) { st = 0; ph ^= 1; }
-            mbar_wait(&bars->in_full[st], ph);
+            mbar_wait(&bars->q_full[qr.i], qr.ph);
             tc_fence_after();
-            nQ = sbase + kQOff + st * kTileBytes;
-            nDO = sbase + kDOOff + st * kTileBytes;
             issue_qk(tS, sK, nQ);  // S^T(i+1): runs after dV(i) read P^T (in order)
             mma_commit(&bars->s_full);
           }
@@ -333,8 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
           ds_ph ^= 1;
           tc_fence_after();
           issue_pv_half(tDK, tDP + 80, sQ, 1, true);
-          mma_commit(&bars->in_empty[cur]);
+          mma_commit(&bars->q_empty[qcur]);   // Q(i): S^T(i), dK(i); its -LSE rows: exps(i)
+          mma_commit(&bars->do_empty[dcur]);  // dO(i): dP^T(i), dV(i); its -D rows: dS(i)
           if (i + 1 < n) {
+            mbar_wait(&bars->do_full[dr.i], dr.ph);
+            tc_fence_after();
             issue_qk(tDP, sV, nDO);  // dP^T(i+1)
             mma_commit(&bars->dp_full);
             sQ = nQ;
@@ -343,7 +383,6 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         }
         mma_commit(&bars->acc_full);
         mma_commit(&bars->kv_empty);
-        if (++st == kStages) { st = 0; ph ^= 1; }
       }
     }
   } else {
@@ -354,7 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
     const uint32_t lsel = ((warp & 3) * 32) << 16;
     const int c0 = 64 * w;
     const uint32_t tSw = tS + lsel, tDPw = tDP + lsel;
-    uint32_t st = 0, ph = 0, s_ph = 0, dp_ph = 0, acc_ph = 0;
+    uint32_t s_ph = 0, dp_ph = 0, acc_ph = 0;
+    KRing<kQStages> qr;
+    KRing<kDOStages> dr;
     for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
       const int u = sched_unit(p.sched, gridDim.x, ui);
       const KvUnit un = p.units[u];
@@ -364,9 +405,12 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
       for (int i = 0; i < un.n_iter; ++i, c.next(un, p.segs, p.group)) {
         const DevTask tk = p.tasks[p.segs[c.seg].task];
         const int shift = tk.kv_len - tk.n_q;
-        mbar_wait_warp(&bars->in_full[st], ph);
-        const uint32_t s_nlse = smem_u32(rows + st * 256), s_nd = s_nlse + 512;
-        if (++st == kStages) { st = 0; ph ^= 1; }
+        mbar_wait_warp(&bars->q_full[qr.i], qr.ph);  // Q(i) and its -LSE rows
+        const uint32_t s_nlse = smem_u32(lse_rows + qr.i * 128), s_nd = smem_u32(d_rows + dr.i * 128);
+        uint64_t* const do_full = &bars->do_full[dr.i];
+        const uint32_t do_ph = dr.ph;
+        qr.next();
+        dr.next();
         mbar_wait_warp(&bars->s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
@@ -434,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_kernel(const __grid_c
         }
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
+        mbar_wait_warp(do_full, do_ph);  // the tile's -D rows
         tc_fence_after();
         float y[64];
         {

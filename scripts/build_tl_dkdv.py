@@ -27,19 +27,23 @@ W = "if (threadIdx.x == 0) "
 rep(r"mbar_wait\(&bars->p_full, p_ph\);", L + "TL(7, tli + i);", L + "TL(0, tli + i);")
 rep(r"mma_commit\(&bars->s_full\);", post=L + "TL(8, tli + i);", nth=1)
 rep(r"mbar_wait\(&bars->ds_full, ds_ph\);", L + "TL(13, tli + i);", L + "TL(1, tli + i);")
-rep(r"mma_commit\(&bars->in_empty\[cur\]\);", post=L + "TL(9, tli + i);")
+rep(r"mma_commit\(&bars->q_empty\[qcur\]\);.*", post=L + "TL(9, tli + i);")
 rep(r"mma_commit\(&bars->dp_full\);", post=L + "TL(10, tli + i);", nth=1)
-rep(r"mbar_wait\(&bars->in_full\[st\], ph\);", L + "TL(11, tli + i);", L + "TL(12, tli + i);", nth=1)
+rep(r"mbar_wait\(&bars->q_full\[qr\.i\], qr\.ph\);", L + "TL(11, tli + i);", L + "TL(12, tli + i);", nth=1)
 W1 = "else if (threadIdx.x == 128) "
 rep(r"mbar_wait_warp\(&bars->s_full, s_ph\);", W + "TL(2, tli + i); " + W1 + "TL(14, tli + i);", W + "TL(3, tli + i); " + W1 + "TL(15, tli + i);")
-rep(r"mbar_arrive\(&bars->p_full\);", post=W + "TL(4, tli + i); " + W1 + "TL(16, tli + i);")
+rep(r"mbar_arrive\(ch \? &bars->p_full : &bars->p_half\);", post="if (ch) { " + W + "TL(4, tli + i); " + W1 + "TL(16, tli + i); }")
 rep(r"mbar_wait_warp\(&bars->dp_full, dp_ph\);", post=W + "TL(5, tli + i); " + W1 + "TL(17, tli + i);")
-rep(r"mbar_arrive\(&bars->ds_full\);", post=W + "TL(6, tli + i); " + W1 + "TL(18, tli + i);")
-loop = "for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {"
-parts = k.split(loop)
+rep(r"mbar_arrive\(ch \? &bars->ds_full : &bars->ds_half\);", post="if (ch) { " + W + "TL(6, tli + i); " + W1 + "TL(18, tli + i); }")
+# trace index = position of the iteration in this CTA's work list
+decl = "const KvUnit un = p.units[u];"
+parts = k.split(decl)
 assert len(parts) == 4, len(parts)  # producer, MMA, elementwise
-k = parts[0] + loop + parts[1] + "int tli = 0;\n" + loop.replace("u += ", "tli += p.units[u].n_iter, u += ") + parts[2] + \
-    "int tli = 0;\n" + loop.replace("u += ", "tli += p.units[u].n_iter, u += ") + parts[3]
+k = parts[0] + decl + parts[1] + decl + " tli = tl_next; tl_next += un.n_iter;" + parts[2] + decl + \
+    " tli = tl_next; tl_next += un.n_iter;" + parts[3]
+k = k.replace("    } else if (warp == 9) {", "    } else if (warp == 9) {\n      int tli = 0, tl_next = 0;", 1)
+k = k.replace('    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");',
+              '    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");\n    int tli = 0, tl_next = 0;', 1)
 s = s[:a] + k + s[b:]
 s += """
 extern "C" int cad_debug_timeline(unsigned long long* out) {
