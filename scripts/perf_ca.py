@@ -28,10 +28,13 @@ F = plan.fwd_flops
 runs = {"fwd": (lambda: plan.forward(q, k, v, o, lse), F),
         "delta": (lambda: plan.backward(q, k, v, o, lse, do, dq, dk, dv, ws, parts=BWD_DELTA), 0),
         "dkdv": (lambda: plan.backward(q, k, v, o, lse, do, dq, dk, dv, ws, parts=BWD_DKDV), 2 * F),
-        "dq": (lambda: plan.backward(q, k, v, o, lse, do, dq, dk, dv, ws, parts=BWD_DQ), 1.5 * F)}
+        "dq": (lambda: plan.backward(q, k, v, o, lse, do, dq, dk, dv, ws, parts=BWD_DQ), 1.5 * F),
+        "bwd": (lambda: plan.backward(q, k, v, o, lse, do, dq, dk, dv, ws), 2.5 * F)}
 st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 tot = 0
 for name, (fn, fl) in runs.items():
+    if name == "bwd":
+        continue
     fn(); torch.cuda.synchronize()
     st.record()
     for _ in range(reps):
@@ -40,4 +43,13 @@ for name, (fn, fl) in runs.items():
     ms = st.elapsed_time(en) / reps
     tot += ms
     print(f"{name:6s} {ms:8.2f} ms  {fl / ms / 1e9 if fl else 0:8.1f} TFLOP/s (executed)")
-print(f"total  {tot:8.2f} ms  {3.5 * F / tot / 1e9:8.1f} TFLOP/s (algorithmic fwd+bwd)")
+print(f"total  {tot:8.2f} ms  {3.5 * F / tot / 1e9:8.1f} TFLOP/s (algorithmic fwd+bwd, parts)")
+fn, fl = runs["bwd"]
+fn(); torch.cuda.synchronize()
+st.record()
+for _ in range(reps):
+    fn()
+en.record(); torch.cuda.synchronize()
+bms = st.elapsed_time(en) / reps
+fms = None
+print(f"bwd    {bms:8.2f} ms  {fl / bms / 1e9:8.1f} TFLOP/s (algorithmic, one call)")
