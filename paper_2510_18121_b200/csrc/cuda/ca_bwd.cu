@@ -32,6 +32,7 @@
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
+#include "ca_rows.cuh"
 #include "sm100.cuh"
 
 namespace cad_dev {
@@ -39,47 +40,6 @@ namespace bwd {
 
 constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
-
-__device__ __forceinline__ void load_row64(uint32_t taddr, float (&x)[64]) {
-  uint32_t r[32];
-  tmem_ld32(taddr, r);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
-  tmem_ld32(taddr + 32, r);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) x[32 + i] = __uint_as_float(r[i]);
-  tmem_wait_ld();
-}
-
-// 64 fp32 -> 32 packed bf16x2 columns at taddr.
-__device__ __forceinline__ void store_bf16_64(uint32_t taddr, const float (&x)[64]) {
-  uint32_t pk[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
-  tmem_st32(taddr, pk);
-}
-
-// Epilogue helper: TMEM row (64 fp32 columns at taddr) * mul -> bf16 -> 128
-// contiguous bytes at dst (if valid).
-__device__ __forceinline__ void tmem_row_to_global(uint32_t taddr, float mul, __nv_bfloat16* dst,
-                                                   bool valid) {
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t r[32];
-    tmem_ld32(taddr + c * 32, r);
-    tmem_wait_ld();
-    uint4 w[4];
-    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * mul, __uint_as_float(r[2 * i + 1]) * mul);
-    if (valid) {
-      uint4* d = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = w[i];
-    }
-  }
-}
 
 // ============================================================== D = rowsum
 // One warp per (row, head): 128 bf16 of dO and O, lanes take 4 each. Stores
@@ -877,8 +837,12 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       cuda_check(cudaGetLastError(), "ca_bwd_dkdv launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv");
     }
-    // 3. dQ
-    if (parts & CAD_BWD_DQ) {
+    // 3. dQ (CTA pairs for even GQA groups unless CAD_DQ_PAIR=0)
+    static const bool dq_pair_off = std::getenv("CAD_DQ_PAIR") && std::getenv("CAD_DQ_PAIR")[0] == '0';
+    if ((parts & CAD_BWD_DQ) && !dq_pair_off &&
+        launch_dq_pair(plan, q, k, v, dout, lse2, delta, pitch, dq, s)) {
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq_pair");
+    } else if (parts & CAD_BWD_DQ) {
       dq::Params p;
       make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
       make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);

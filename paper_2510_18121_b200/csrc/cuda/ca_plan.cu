@@ -95,6 +95,9 @@ static void build_units(cad_ca_plan& P) {
           P.fwd_units.push_back({t, i, static_cast<int16_t>(hk * group + g), static_cast<int16_t>(per_unit), n_kv});
         for (int g = 0; g < group; ++g)
           P.dq_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 1, n_kv});
+        if (group % 2 == 0)
+          for (int g = 0; g < group; g += 2)
+            P.dq2_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 2, n_kv});
         if (group % 4 == 0)
           for (int g = 0; g < group; g += 4)
             P.fwd2_units.push_back({t, i, static_cast<int16_t>(hk * group + g), 4, n_kv});
@@ -158,6 +161,10 @@ static void build_units(cad_ca_plan& P) {
     const int ha = a.head0 / group, hb = b.head0 / group;
     return ha != hb ? ha < hb : a.n_kv > b.n_kv;
   });
+  std::stable_sort(P.dq2_units.begin(), P.dq2_units.end(), [group](const FwdUnit& a, const FwdUnit& b) {
+    const int ha = a.head0 / group, hb = b.head0 / group;
+    return ha != hb ? ha < hb : a.n_kv > b.n_kv;
+  });
   std::stable_sort(P.kv_units.begin(), P.kv_units.end(), [](const KvUnit& a, const KvUnit& b) {
     return a.hk != b.hk ? a.hk < b.hk : a.n_iter > b.n_iter;
   });
@@ -201,6 +208,8 @@ static void build_schedules(cad_ca_plan& P) {
   deal(P.sched_fwd2, fwd_cost(P.fwd2_units),
        std::max<int>(1, std::min<int64_t>(P.fwd2_units.size(), P.grid(1 << 30) / 2)));
   deal(P.sched_dq, fwd_cost(P.dq_units), P.grid(P.dq_units.size()));
+  deal(P.sched_dq2, fwd_cost(P.dq2_units),
+       std::max<int>(1, std::min<int64_t>(P.dq2_units.size(), P.grid(1 << 30) / 2)));
   c.clear();
   const int group = P.shape.h_q / P.shape.h_kv;
   for (const KvUnit& u : P.kv_units) c.push_back(int64_t(u.n_iter) + 2 * group);
@@ -253,6 +262,7 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     upload(P->fwd_units, &P->d_fwd);
     upload(P->dq_units, &P->d_dq);
     upload(P->fwd2_units, &P->d_fwd2);
+    upload(P->dq2_units, &P->d_dq2);
     upload(P->kv_units, &P->d_kv);
     upload(P->kv_segs, &P->d_segs);
     cad_dev::build_schedules(*P);
@@ -290,9 +300,11 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     cudaFree(plan->d_fwd);
     cudaFree(plan->d_dq);
     cudaFree(plan->d_fwd2);
+    cudaFree(plan->d_dq2);
     cudaFree(plan->d_kv);
     cudaFree(plan->d_segs);
-    for (cad_dev::CtaLists* L : {&plan->sched_fwd, &plan->sched_fwd2, &plan->sched_dq, &plan->sched_kv})
+    for (cad_dev::CtaLists* L : {&plan->sched_fwd, &plan->sched_fwd2, &plan->sched_dq, &plan->sched_dq2,
+                                 &plan->sched_kv})
       cudaFree(L->d);
     delete plan;
   });

@@ -1,0 +1,53 @@
+// TMEM row helpers shared by the backward kernels (thread = TMEM lane =
+// tile row): 64-column loads, bf16 packing back into TMEM, and the epilogue
+// store of an accumulator row to global memory.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "sm100.cuh"
+
+namespace cad_dev {
+
+__device__ __forceinline__ void load_row64(uint32_t taddr, float (&x)[64]) {
+  uint32_t r[32];
+  tmem_ld32(taddr, r);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+  tmem_ld32(taddr + 32, r);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[32 + i] = __uint_as_float(r[i]);
+  tmem_wait_ld();
+}
+
+// 64 fp32 -> 32 packed bf16x2 columns at taddr.
+__device__ __forceinline__ void store_bf16_64(uint32_t taddr, const float (&x)[64]) {
+  uint32_t pk[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
+  tmem_st32(taddr, pk);
+}
+
+// Epilogue helper: TMEM row (64 fp32 columns at taddr) * mul -> bf16 -> 128
+// contiguous bytes at dst (if valid).
+__device__ __forceinline__ void tmem_row_to_global(uint32_t taddr, float mul, __nv_bfloat16* dst,
+                                                   bool valid) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    uint4 w[4];
+    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * mul, __uint_as_float(r[2 * i + 1]) * mul);
+    if (valid) {
+      uint4* d = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = w[i];
+    }
+  }
+}
+
+}  // namespace cad_dev
