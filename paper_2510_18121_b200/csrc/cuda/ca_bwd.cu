@@ -811,8 +811,12 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       cuda_check(cudaGetLastError(), "ca_delta launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
     }
-    // 2. dK, dV
-    if ((parts & CAD_BWD_DKDV) && !plan->kv_units.empty()) {
+    // 2. dK, dV (CTA pairs unless CAD_DKDV_PAIR=0)
+    static const bool dkdv_pair_off = std::getenv("CAD_DKDV_PAIR") && std::getenv("CAD_DKDV_PAIR")[0] == '0';
+    if ((parts & CAD_BWD_DKDV) && !dkdv_pair_off &&
+        launch_dkdv_pair(plan, q, k, v, dout, lse2, delta, pitch, dk, dv, s)) {
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdv_pair");
+    } else if ((parts & CAD_BWD_DKDV) && !plan->kv_units.empty()) {
       kv::Params p;
       make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
       make_tile_map(&p.tm_do, dout, sh.q_rows, sh.h_q);

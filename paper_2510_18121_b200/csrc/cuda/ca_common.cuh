@@ -72,6 +72,7 @@ struct cad_ca_plan {
   std::vector<cad_dev::FwdUnit> fwd2_units;  // CTA-pair forward: nh == 4 (GQA group % 4 == 0)
   std::vector<cad_dev::FwdUnit> dq2_units;   // CTA-pair dQ: nh == 2 (even GQA group)
   std::vector<cad_dev::KvUnit> kv_units;
+  std::vector<cad_dev::KvUnit> kv2_units;  // CTA-pair dK/dV: kv tiles (tile, tile + 1)
   std::vector<cad_dev::KvSeg> kv_segs;
   cad_dev::DevTask* d_tasks = nullptr;
   cad_dev::FwdUnit* d_fwd = nullptr;
@@ -79,6 +80,7 @@ struct cad_ca_plan {
   cad_dev::FwdUnit* d_fwd2 = nullptr;
   cad_dev::FwdUnit* d_dq2 = nullptr;
   cad_dev::KvUnit* d_kv = nullptr;
+  cad_dev::KvUnit* d_kv2 = nullptr;
   cad_dev::KvSeg* d_segs = nullptr;
   int64_t pairs = 0;
   int device = 0;
@@ -89,7 +91,7 @@ struct cad_ca_plan {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(units, cap)));
   }
   // LPT work lists per kernel for the current grid (rebuilt by set_max_ctas)
-  cad_dev::CtaLists sched_fwd, sched_fwd2, sched_dq, sched_dq2, sched_kv;
+  cad_dev::CtaLists sched_fwd, sched_fwd2, sched_dq, sched_dq2, sched_kv, sched_kv2;
 };
 
 namespace cad_dev {
@@ -103,6 +105,9 @@ void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
 void cuda_check(cudaError_t e, const char* what);
 bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
                      cudaStream_t stream);
+bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
+                      const float* nlse2, const float* ndelta, int64_t pitch, void* dk, void* dv,
+                      cudaStream_t stream);
 bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
                     const float* lse2, const float* delta, int64_t pitch, void* dq, cudaStream_t stream);
 

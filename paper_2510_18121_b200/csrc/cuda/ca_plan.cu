@@ -165,7 +165,15 @@ static void build_units(cad_ca_plan& P) {
     const int ha = a.head0 / group, hb = b.head0 / group;
     return ha != hb ? ha < hb : a.n_kv > b.n_kv;
   });
+  // CTA-pair dK/dV: the even kv tiles of every group; the pair's second tile
+  // (tile + 1, possibly past kv_end) is seen by a subset of the first one's
+  // q tiles, so the first tile's segments and length cover both.
+  for (const KvUnit& u : P.kv_units)
+    if (u.tile % 2 == 0) P.kv2_units.push_back(u);
   std::stable_sort(P.kv_units.begin(), P.kv_units.end(), [](const KvUnit& a, const KvUnit& b) {
+    return a.hk != b.hk ? a.hk < b.hk : a.n_iter > b.n_iter;
+  });
+  std::stable_sort(P.kv2_units.begin(), P.kv2_units.end(), [](const KvUnit& a, const KvUnit& b) {
     return a.hk != b.hk ? a.hk < b.hk : a.n_iter > b.n_iter;
   });
 }
@@ -214,6 +222,9 @@ static void build_schedules(cad_ca_plan& P) {
   const int group = P.shape.h_q / P.shape.h_kv;
   for (const KvUnit& u : P.kv_units) c.push_back(int64_t(u.n_iter) + 2 * group);
   deal(P.sched_kv, c, P.grid(P.kv_units.size()));
+  c.clear();
+  for (const KvUnit& u : P.kv2_units) c.push_back(int64_t(u.n_iter) + 2 * group);
+  deal(P.sched_kv2, c, std::max<int>(1, std::min<int64_t>(P.kv2_units.size(), P.grid(1 << 30) / 2)));
 }
 
 }  // namespace cad_dev
@@ -264,6 +275,7 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     upload(P->fwd2_units, &P->d_fwd2);
     upload(P->dq2_units, &P->d_dq2);
     upload(P->kv_units, &P->d_kv);
+    upload(P->kv2_units, &P->d_kv2);
     upload(P->kv_segs, &P->d_segs);
     cad_dev::build_schedules(*P);
     *plan = P.release();
@@ -302,9 +314,10 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     cudaFree(plan->d_fwd2);
     cudaFree(plan->d_dq2);
     cudaFree(plan->d_kv);
+    cudaFree(plan->d_kv2);
     cudaFree(plan->d_segs);
     for (cad_dev::CtaLists* L : {&plan->sched_fwd, &plan->sched_fwd2, &plan->sched_dq, &plan->sched_dq2,
-                                 &plan->sched_kv})
+                                 &plan->sched_kv, &plan->sched_kv2})
       cudaFree(L->d);
     delete plan;
   });
