@@ -53,3 +53,21 @@ def test_bwd_matches_oracle(name):
     res = run_bwd(tasks, rows, rows, h_q, h_kv)
     for g, (err, mag) in res.items():
         assert err <= TOL * max(1.0, mag), f"{g}: max abs err {err} (max |ref| {mag})"
+
+
+def test_single_cta_kernels_match_oracle():
+    """The single-CTA dK/dV and dQ kernels (the CTA-pair ones are the
+    default) on every case, in a fresh process so the switches take effect."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    env = dict(os.environ, CAD_DKDV_PAIR="0", CAD_DQ_PAIR="0", CAD_FWD_PAIR="0",
+               PYTHONPATH=os.pathsep.join([root, here, os.environ.get("PYTHONPATH", "")]))
+    code = ("import test_ca_bwd_gpu as t\n"
+            "for n in sorted(t.CASES): t.test_bwd_matches_oracle(n)\n"
+            "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=here, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
