@@ -77,20 +77,8 @@ __device__ __forceinline__ void issue_qk_pair(uint32_t d_tmem, uint32_t q_smem, 
   }
 }
 
-// O += P V, M=256, N=128 d (64 per CTA: one MN-major plane), K=128 kv rows.
-__device__ __forceinline__ void issue_pv_pair(uint32_t d_tmem, uint32_t p_lo, uint32_t p_hi, uint32_t v_smem,
-                                              bool accumulate) {
-  constexpr uint32_t idesc = idesc_bf16(256, 128, false, true);
-  if (!elect_one()) return;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t a = k < 4 ? p_lo + k * 8 : p_hi + (k - 4) * 8;
-    umma_ts_2sm(d_tmem, a, sw128_desc(v_smem + k * 2048, kHalfBytes, 1024), idesc,
-                (accumulate || k > 0) ? 1u : 0u);
-  }
-}
-
-// One K-half (kv rows [64*half, 64*half+64)) of issue_pv_pair.
+// O += P V for one K-half (kv rows [64*half, 64*half+64)): M=256, N=128 d
+// (64 per CTA: one MN-major plane); P from TMEM.
 __device__ __forceinline__ void issue_pv_pair_half(uint32_t d_tmem, uint32_t p, uint32_t v_smem, int half,
                                                    bool accumulate) {
   constexpr uint32_t idesc = idesc_bf16(256, 128, false, true);

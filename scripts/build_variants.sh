@@ -7,7 +7,7 @@ mkdir -p lib/variants /tmp/cadvar
 # each argument: NAME:NVCC_DEFINES (comma separated), e.g. st5:CAD_FWD2_STAGES=5
 for spec in "$@"; do
   m=${spec%%:*}; defs=$(echo "${spec#*:}" | tr ',' '\n' | sed 's/^/-D/' | tr '\n' ' ')
-  for k in ca_fwd ca_fwd2 ca_bwd; do
+  for k in ca_fwd ca_fwd2 ca_bwd ca_dkdv2 ca_dq2; do
     nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
       --expt-relaxed-constexpr $defs -c csrc/cuda/$k.cu -o /tmp/cadvar/${k}_$m.o &
   done
@@ -15,7 +15,7 @@ done
 wait
 for spec in "$@"; do
   m=${spec%%:*}
-  objs=$(ls build/*.o | grep -v -E "cuda_ca_(fwd2?|bwd)\.o")
+  objs=$(ls build/*.o | grep -v -E "cuda_ca_(fwd2?|bwd|dkdv2|dq2)\.o")
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o lib/variants/libcad_$m.so $objs \
-    /tmp/cadvar/ca_fwd_$m.o /tmp/cadvar/ca_fwd2_$m.o /tmp/cadvar/ca_bwd_$m.o -ldl -lpthread
+    /tmp/cadvar/ca_fwd_$m.o /tmp/cadvar/ca_fwd2_$m.o /tmp/cadvar/ca_bwd_$m.o /tmp/cadvar/ca_dkdv2_$m.o /tmp/cadvar/ca_dq2_$m.o -ldl -lpthread
 done
