@@ -1,5 +1,5 @@
 """Per-kernel times on BASELINE config 2 (8B shape, 128K tokens, seed 1):
-fwd, delta, dK/dV, dQ. Usage: perf_ca.py [reps]."""
+fwd, delta, dK/dV, dQ. Usage: perf_ca.py [reps] [only,these,parts]."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -7,6 +7,7 @@ from paper_2510_18121_b200 import scheduler as S
 from paper_2510_18121_b200.ca import CAPlan, CATaskRows, BWD_DELTA, BWD_DKDV, BWD_DQ
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 hq, hkv = 32, 8
 d = S.LengthDistribution(kind=S.PRETRAIN_UPSAMPLED, max_doc_len=131072, min_len_threshold=32768,
                          upsample_drop_prob=0.9, seed=1)
@@ -33,7 +34,7 @@ runs = {"fwd": (lambda: plan.forward(q, k, v, o, lse), F),
 st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 tot = 0
 for name, (fn, fl) in runs.items():
-    if name == "bwd":
+    if name == "bwd" or (only and name not in only):
         continue
     fn(); torch.cuda.synchronize()
     st.record()
@@ -44,6 +45,8 @@ for name, (fn, fl) in runs.items():
     tot += ms
     print(f"{name:6s} {ms:8.2f} ms  {fl / ms / 1e9 if fl else 0:8.1f} TFLOP/s (executed)")
 print(f"total  {tot:8.2f} ms  {3.5 * F / tot / 1e9:8.1f} TFLOP/s (algorithmic fwd+bwd, parts)")
+if only and "bwd" not in only:
+    sys.exit(0)
 fn, fl = runs["bwd"]
 fn(); torch.cuda.synchronize()
 st.record()
