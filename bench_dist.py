@@ -19,6 +19,9 @@ import torch
 import torch.distributed as dist
 
 
+_WORKLOADS = {"cfg3": "BASELINE config 3", "cfg4": "BASELINE config 4", "cfg5": "BASELINE config 5 (imbalance sweep)"}
+
+
 def _timed(fn, steps, stream):
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
@@ -46,9 +49,22 @@ def run(args, metric, load_peaks, ClockSampler):
     from paper_2510_18121_b200 import dispatch as D
     from paper_2510_18121_b200 import scheduler as S
 
-    shape = CF.LLAMA8B
-    per_gpu = 65536
-    lengths = S.sample_batch(CF.length_dist("pretrain", 1), per_gpu * world)
+    # CAD_WORKLOAD: cfg3 (default; 8B, 64K tokens per GPU, weak scaling),
+    # cfg4 (34B, 64 Q / 8 KV heads, 1M tokens over the N GPUs: strong
+    # scaling, docs up to 256K) or cfg5-<uniform|lognormal|prolong|fixed>
+    # (the imbalance sweep's distributions at the config-3 shape)
+    workload = os.environ.get("CAD_WORKLOAD", "cfg3")
+    seed = int(os.environ.get("CAD_SEED", "1"))
+    if workload == "cfg4":
+        shape, total, scaling = CF.LLAMA34B, 1 << 20, "strong"
+        dist_ = CF.length_dist("pretrain", seed, max_doc_len=262144)
+    elif workload == "cfg3" or workload.startswith("cfg5-"):
+        shape, total, scaling = CF.LLAMA8B, 65536 * world, "weak"
+        dist_ = CF.length_dist("pretrain" if workload == "cfg3" else workload[5:], seed)
+    else:
+        raise ValueError(f"unknown CAD_WORKLOAD {workload!r}")
+    per_gpu = total // world
+    lengths = S.sample_batch(dist_, total)
     lp = D.LayerPlan(lengths, world, rank, shape)
     obj = [D.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
@@ -79,7 +95,7 @@ def run(args, metric, load_peaks, ClockSampler):
     comp = torch.cuda.current_stream(dev)
     # stacked CA layers per step (copy-engine transport): the dispatch of
     # layer l+1 and the return of layer l overlap the other half's CA
-    layers = int(os.environ.get("CAD_LAYERS", "4")) if transport == "ce" else 1
+    layers = int(os.environ.get("CAD_LAYERS", "1" if workload == "cfg4" else "4")) if transport == "ce" else 1
     if transport == "ce":
         layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq,
                                layers=layers, copy_mode=copy_mode, copy_ctas=copy_ctas)
@@ -164,14 +180,15 @@ def run(args, metric, load_peaks, ClockSampler):
             naive_pairs.append(sum(S.exact_causal_pairs(it.q_end - it.q_begin, it.q_end) for it in its))
         out = {
             "metric": metric, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"BASELINE config 3 shape: Llama-3-8B CA (32 Q / 8 KV), {per_gpu} tokens per GPU "
-                                   f"({per_gpu * world} total), pretrain_upsampled seed 1, scheduler-sharded, "
+            "config": {"workload": f"{_WORKLOADS[workload.split('-')[0]]}: {shape.name} CA ({shape.h_q} Q / {shape.h_kv} KV), "
+                                   f"{per_gpu} tokens per GPU ({total} total), "
+                                   f"{'pretrain_upsampled' if workload in ('cfg3', 'cfg4') else workload[5:]} lengths seed {seed}, scheduler-sharded, "
                                    f"{'copy-engine (CUDA IPC) pushes' if transport == 'ce' else 'NCCL all-to-allv'} dispatch/return, "
                                    f"ping-pong halves, {layers} stacked CA layer(s) fwd+bwd per step "
                                    "(identity between layers)",
-                       "layers_per_step": layers,
+                       "workload_id": workload, "layers_per_step": layers,
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
                        "parallelism": f"CA servers x{world} (scheduler sharding)",
