@@ -1,0 +1,138 @@
+"""CA forward + backward at BASELINE config 2's full size (Llama-3-8B shape,
+32 Q / 8 KV heads, 128K packed tokens, pretrain_upsampled seed 1: docs up to
+~100K tokens) on the B200, checked through size-independent properties:
+
+* sampled rows against a float64 restatement of the CA math (PAPER.md:129,
+  bottom-right causal mask of P/src/oracle.cpp:50-54): O and LSE of a query
+  row need only that row and its document's keys; dQ of a row additionally
+  D = rowsum(dO * O); dK/dV of a key row are sums over the query rows that
+  see it, with P recomputed from the kernel's LSE (validated on the sampled
+  rows) -- the same recompute the backward does;
+* composability: the longest document split into query
+  shards (tile-aligned and unaligned cuts) gives the whole-document rows.
+
+Tolerances as in the small-case tests: O 2e-2, LSE 1e-3, gradients 2e-2 x
+max(1, max |ref|).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+O_TOL, LSE_TOL, G_TOL = 2e-2, 1e-3, 2e-2
+
+
+@pytest.fixture(scope="module")
+def full():
+    from paper_2510_18121_b200 import configs as CF
+    from paper_2510_18121_b200 import scheduler as S
+    from paper_2510_18121_b200.ca import CAPlan, CATaskRows
+    lengths = S.sample_batch(CF.length_dist("pretrain", 1), 131072)
+    starts = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    T, hq, hkv = int(sum(lengths)), 32, 8
+    tasks = [CATaskRows(int(s), int(l), int(s), int(l)) for s, l in zip(starts, lengths)]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    bf = dict(device="cuda", dtype=torch.bfloat16)
+    q = torch.randn(T, hq, 128, generator=g, **bf)
+    k = torch.randn(T, hkv, 128, generator=g, **bf)
+    v = torch.randn(T, hkv, 128, generator=g, **bf)
+    do = torch.randn(T, hq, 128, generator=g, **bf)
+    plan = CAPlan(tasks, hq, hkv, T, T)
+    o, lse = plan.forward(q, k, v)
+    dq, dk, dv = plan.backward(q, k, v, o, lse, do)
+    torch.cuda.synchronize()
+    return dict(lengths=list(lengths), starts=starts, q=q, k=k, v=v, do=do, o=o, lse=lse, dq=dq, dk=dk, dv=dv,
+                hq=hq, hkv=hkv, T=T, tasks=tasks)
+
+
+def _doc_of(f, row):
+    d = int(np.searchsorted(f["starts"], row, side="right") - 1)
+    return d, int(f["starts"][d]), int(f["starts"][d] + f["lengths"][d])
+
+
+def _sample_rows(f, n, rng):
+    rows = set()
+    for d, (s, l) in enumerate(zip(f["starts"], f["lengths"])):
+        rows.update({int(s), int(s + l - 1), int(s + min(l - 1, 127)), int(s + min(l - 1, 128))})
+    rows.update(int(x) for x in rng.integers(0, f["T"], n))
+    return sorted(rows)
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def test_full_size_rows_match_float64(full):
+    f = full
+    rng = np.random.default_rng(5)
+    scale = 1.0 / np.sqrt(128.0)
+    group = f["hq"] // f["hkv"]
+    worst = {"o": 0.0, "lse": 0.0, "dq": 0.0}
+    for row in _sample_rows(f, 12, rng):
+        _, s, _ = _doc_of(f, row)
+        h = int(rng.integers(0, f["hq"]))
+        hk = h // group
+        K, V = _np(f["k"][s:row + 1, hk]), _np(f["v"][s:row + 1, hk])
+        qi, doi, oi = _np(f["q"][row, h]), _np(f["do"][row, h]), _np(f["o"][row, h])
+        sc = K @ qi * scale
+        m = sc.max()
+        lse = m + np.log(np.exp(sc - m).sum())
+        p = np.exp(sc - lse)
+        o_ref = p @ V
+        worst["o"] = max(worst["o"], np.abs(o_ref - _np(f["o"][row, h])).max())
+        worst["lse"] = max(worst["lse"], abs(lse - float(f["lse"][h, row])))
+        dp = V @ doi
+        ds = p * (dp - doi @ oi)
+        dq_ref = scale * (ds @ K)
+        worst["dq"] = max(worst["dq"], np.abs(dq_ref - _np(f["dq"][row, h])).max() / max(1.0, np.abs(dq_ref).max()))
+    print("full-size query rows, worst errors:", worst)
+    assert worst["o"] <= O_TOL, worst
+    assert worst["lse"] <= LSE_TOL, worst
+    assert worst["dq"] <= G_TOL, worst
+
+
+def test_full_size_kv_rows_match_float64(full):
+    f = full
+    rng = np.random.default_rng(6)
+    scale = 1.0 / np.sqrt(128.0)
+    group = f["hq"] // f["hkv"]
+    big = int(np.argmax(f["lengths"]))
+    s0, l0 = int(f["starts"][big]), int(f["lengths"][big])
+    # key rows of the longest document (early rows see ~all its queries) + random ones
+    rows = [s0, s0 + 1, s0 + 127, s0 + 128, s0 + l0 // 2, s0 + l0 - 1] + [int(x) for x in rng.integers(0, f["T"], 3)]
+    worst = {"dk": 0.0, "dv": 0.0}
+    for j in rows:
+        _, s, e = _doc_of(f, j)
+        hk = int(rng.integers(0, f["hkv"]))
+        kj, vj = _np(f["k"][j, hk]), _np(f["v"][j, hk])
+        dk_ref, dv_ref = np.zeros(128), np.zeros(128)
+        for h in range(hk * group, (hk + 1) * group):
+            Q, dO, O = _np(f["q"][j:e, h]), _np(f["do"][j:e, h]), _np(f["o"][j:e, h])
+            lse = f["lse"][h, j:e].double().cpu().numpy()
+            p = np.exp(Q @ kj * scale - lse)
+            dv_ref += p @ dO
+            ds = p * (dO @ vj - (dO * O).sum(1))
+            dk_ref += scale * (ds @ Q)
+        worst["dk"] = max(worst["dk"], np.abs(dk_ref - _np(f["dk"][j, hk])).max() / max(1.0, np.abs(dk_ref).max()))
+        worst["dv"] = max(worst["dv"], np.abs(dv_ref - _np(f["dv"][j, hk])).max() / max(1.0, np.abs(dv_ref).max()))
+    print("full-size key rows, worst relative errors:", worst)
+    assert worst["dk"] <= G_TOL, worst
+    assert worst["dv"] <= G_TOL, worst
+
+
+def test_full_size_split_longest_doc_equals_whole(full):
+    from paper_2510_18121_b200.ca import CAPlan, CATaskRows
+    f = full
+    big = int(np.argmax(f["lengths"]))
+    s0, l0 = int(f["starts"][big]), int(f["lengths"][big])
+    cuts = sorted({128 * (l0 // 512), l0 // 3, 128 * (l0 // 256) + 77, l0 - 1})
+    bounds = [0] + [c for c in cuts if 0 < c < l0] + [l0]
+    tasks = [t for i, t in enumerate(f["tasks"]) if i != big]
+    tasks += [CATaskRows(s0 + a, b - a, s0, b) for a, b in zip(bounds[:-1], bounds[1:])]
+    plan = CAPlan(tasks, f["hq"], f["hkv"], f["T"], f["T"])
+    o2, lse2 = plan.forward(f["q"], f["k"], f["v"])
+    torch.cuda.synchronize()
+    sl = slice(s0, s0 + l0)
+    assert (o2[sl].float() - f["o"][sl].float()).abs().max().item() <= 1e-2
+    assert (lse2[:, sl] - f["lse"][:, sl]).abs().max().item() <= 1e-4
