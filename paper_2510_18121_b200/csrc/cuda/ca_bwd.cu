@@ -42,42 +42,59 @@ constexpr int kThreads = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ============================================================== D = rowsum
-// One warp per (row, head): 128 bf16 of dO and O, lanes take 4 each. Stores
-// -D and the forward's LSE as -LSE*log2(e) in [h_q][pitch] rows (negated so
-// the consumers fold them into one FFMA2/FADD2).
-__global__ void ca_delta_kernel(const DevTask* tasks, int n_tasks, const __nv_bfloat16* o,
-                                const __nv_bfloat16* dout, const float* lse, float* delta,
-                                float* lse2, int h_q, int64_t q_rows, int64_t pitch) {
-  const int warps_per_block = blockDim.x / 32;
-  const int64_t gw = int64_t(blockIdx.x) * warps_per_block + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  // rows are enumerated task by task
-  int64_t rem = gw / h_q;
-  const int h = static_cast<int>(gw % h_q);
-  for (int t = 0; t < n_tasks; ++t) {
-    if (rem < tasks[t].n_q) {
-      const int64_t row = tasks[t].q_off + rem;
-      const int64_t base = (row * h_q + h) * kHeadDim + lane * 4;
-      const uint2 a = *reinterpret_cast<const uint2*>(o + base);
-      const uint2 b = *reinterpret_cast<const uint2*>(dout + base);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+// One CTA per chunk of <= 32 consecutive query rows of a task, all heads:
+// half-warps take (row, head) pairs in memory order (16-byte loads of the
+// 256-byte dO and O head rows, fully coalesced), the sums go through shared
+// memory, and -D plus the forward's LSE as -LSE*log2(e) are written as
+// 128-byte runs of the [h_q][pitch] rows (negated so the consumers fold them
+// into one FFMA2/FADD2). HBM-bound: 2 x 256 B read per (row, head).
+constexpr int kDeltaThreads = 256;
+__global__ void __launch_bounds__(kDeltaThreads) ca_delta_kernel(const int2* chunks, const __nv_bfloat16* o,
+                                                                 const __nv_bfloat16* dout, const float* lse,
+                                                                 float* delta, float* lse2, int h_q, int64_t q_rows,
+                                                                 int64_t pitch) {
+  extern __shared__ float dsum[];  // [h_q][32]
+  const int2 ch = chunks[blockIdx.x];
+  const int hw = threadIdx.x >> 4, l16 = threadIdx.x & 15;
+  const int items = ch.y * h_q;
+  const uint4* o4 = reinterpret_cast<const uint4*>(o + int64_t(ch.x) * h_q * kHeadDim);
+  const uint4* d4 = reinterpret_cast<const uint4*>(dout + int64_t(ch.x) * h_q * kHeadDim);
+  constexpr int kU = 4;
+  for (int base = hw; base < items; base += kU * (kDeltaThreads / 16)) {
+    uint4 a[kU], b[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int it = base + u * (kDeltaThreads / 16);
+      if (it < items) {
+        a[u] = __ldg(o4 + int64_t(it) * 16 + l16);
+        b[u] = __ldg(d4 + int64_t(it) * 16 + l16);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int it = base + u * (kDeltaThreads / 16);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b[u]);
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const float2 fa = __bfloat1622float2(a2[i]);
         const float2 fb = __bfloat1622float2(b2[i]);
         s += fa.x * fb.x + fa.y * fb.y;
       }
 #pragma unroll
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) {
-        delta[int64_t(h) * pitch + row] = -s;
-        lse2[int64_t(h) * pitch + row] = -lse[int64_t(h) * q_rows + row] * kLog2e;
-      }
-      return;
+      for (int off = 8; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (l16 == 0 && it < items) dsum[(it % h_q) * 32 + it / h_q] = s;
     }
-    rem -= tasks[t].n_q;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < h_q * 32; i += kDeltaThreads) {
+    const int h = i >> 5, r = i & 31;
+    if (r < ch.y) {
+      const int64_t row = ch.x + r;
+      delta[int64_t(h) * pitch + row] = -dsum[i];
+      lse2[int64_t(h) * pitch + row] = -lse[int64_t(h) * q_rows + row] * kLog2e;
+    }
   }
 }
 
@@ -800,14 +817,10 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       attr_set = true;
     }
     // 1. D = rowsum(dO * O)
-    if (parts & CAD_BWD_DELTA) {
-      int64_t rows = 0;
-      for (const DevTask& t : plan->tasks) rows += t.n_q;
-      const int64_t warps = rows * sh.h_q;
-      const int per_block = 8;
-      ca_delta_kernel<<<static_cast<unsigned>((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
-          plan->d_tasks, static_cast<int>(plan->tasks.size()), static_cast<const __nv_bfloat16*>(o),
-          static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, sh.h_q, sh.q_rows, pitch);
+    if ((parts & CAD_BWD_DELTA) && !plan->row_chunks.empty()) {
+      ca_delta_kernel<<<static_cast<unsigned>(plan->row_chunks.size()), kDeltaThreads, sh.h_q * 32 * 4, s>>>(
+          plan->d_row_chunks, static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
+          delta, lse2, sh.h_q, sh.q_rows, pitch);
       cuda_check(cudaGetLastError(), "ca_delta launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
     }

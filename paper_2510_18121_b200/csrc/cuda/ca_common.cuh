@@ -74,7 +74,9 @@ struct cad_ca_plan {
   std::vector<cad_dev::KvUnit> kv_units;
   std::vector<cad_dev::KvUnit> kv2_units;  // CTA-pair dK/dV: kv tiles (tile, tile + 1)
   std::vector<cad_dev::KvSeg> kv_segs;
+  std::vector<int2> row_chunks;  // (first row, rows <= 32) covering every task's query rows
   cad_dev::DevTask* d_tasks = nullptr;
+  int2* d_row_chunks = nullptr;
   cad_dev::FwdUnit* d_fwd = nullptr;
   cad_dev::FwdUnit* d_dq = nullptr;
   cad_dev::FwdUnit* d_fwd2 = nullptr;

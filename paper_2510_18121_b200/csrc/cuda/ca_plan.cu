@@ -269,7 +269,10 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
         cuda_check(cudaMemcpy(*dst, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice),
                    "cudaMemcpy(plan)");
     };
+    for (const cad_dev::DevTask& t : P->tasks)
+      for (int r = 0; r < t.n_q; r += 32) P->row_chunks.push_back(make_int2(t.q_off + r, std::min(32, t.n_q - r)));
     upload(P->tasks, &P->d_tasks);
+    upload(P->row_chunks, &P->d_row_chunks);
     upload(P->fwd_units, &P->d_fwd);
     upload(P->dq_units, &P->d_dq);
     upload(P->fwd2_units, &P->d_fwd2);
@@ -309,6 +312,7 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
   return cad::guarded([&] {
     if (!plan) return;
     cudaFree(plan->d_tasks);
+    cudaFree(plan->d_row_chunks);
     cudaFree(plan->d_fwd);
     cudaFree(plan->d_dq);
     cudaFree(plan->d_fwd2);

@@ -9,9 +9,9 @@ from paper_2510_18121_b200.ca import CAPlan, CATaskRows, BWD_DELTA, BWD_DKDV, BW
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 hq, hkv = 32, 8
-d = S.LengthDistribution(kind=S.PRETRAIN_UPSAMPLED, max_doc_len=131072, min_len_threshold=32768,
-                         upsample_drop_prob=0.9, seed=1)
-lengths = S.sample_batch(d, 131072)
+from paper_2510_18121_b200 import configs as CF
+# CAD_PERF_DIST: pretrain (config 2, default) or a config-5 distribution
+lengths = S.sample_batch(CF.length_dist(os.environ.get("CAD_PERF_DIST", "pretrain"), 1), 131072)
 tasks, off = [], 0
 for l in lengths:
     tasks.append(CATaskRows(off, l, off, l)); off += l
