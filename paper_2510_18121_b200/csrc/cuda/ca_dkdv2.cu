@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_pair_kernel(const __g
         tc_fence_after();
         issue_kq_pair(tDP, sV, sDO);
         commit_pair(&bars->dp_full);
+        if (n == 1) commit_pair(&bars->kv_empty);  // K / V read for the last time
         for (int i = 0; i < n; ++i) {
           const uint32_t qcur = qr.i, dcur = dr.i;
           qr.next();
@@ -300,12 +301,14 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_pair_kernel(const __g
             tc_fence_after();
             issue_kq_pair(tDP, sV, nDO);  // dP^T(i+1)
             commit_pair(&bars->dp_full);
+            // last reads of K / V issued: the next unit's tiles load under
+            // this unit's last element-wise phase, dV/dK MMAs and epilogue
+            if (i + 2 == n) commit_pair(&bars->kv_empty);
             sQ = nQ;
             sDO = nDO;
           }
         }
         commit_pair(&bars->acc_full);
-        commit_pair(&bars->kv_empty);
       }
     }
   } else {

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         commit_pair(&bars->dp_full);
         commit_pair(&bars->v_empty[vr.i]);
         vr.next();
+        if (n == 1) commit_pair(&bars->q_empty);  // Q / dO read for the last time
         for (int j = 0; j < n; ++j) {
           const uint32_t kcur = kr.i;
           kr.next();
@@ -230,6 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
             commit_pair(&bars->dp_full);
             commit_pair(&bars->v_empty[vr.i]);
             vr.next();
+            // last reads of Q / dO issued: the next unit's tiles load under
+            // this unit's last exponentials, dQ MMA and epilogue
+            if (j + 2 == n) commit_pair(&bars->q_empty);
           }
           mbar_wait(&bars->ds_full, ds_ph);
           ds_ph ^= 1;
@@ -243,7 +247,6 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
           commit_pair(&bars->k_empty[kcur]);
         }
         commit_pair(&bars->dq_full);
-        commit_pair(&bars->q_empty);
       }
     }
   } else {
