@@ -22,6 +22,8 @@
 #include <mutex>
 #include <type_traits>
 #include <numeric>
+#include <cstdio>
+#include <cstdlib>
 #include <queue>
 #include <string>
 
@@ -191,6 +193,18 @@ static void deal(CtaLists& L, const std::vector<int64_t>& cost, int G) {
     per[s.second].push_back(static_cast<int32_t>(u));
     s.first += cost[u];
     heap.push(s);
+  }
+  if (std::getenv("CAD_SCHED_STATS")) {
+    std::vector<int64_t> load(G, 0);
+    int64_t tot = 0, mx = 0;
+    for (int c = 0; c < G; ++c) {
+      for (int32_t u : per[c]) load[c] += cost[u];
+      tot += load[c];
+      mx = std::max(mx, load[c]);
+    }
+    const int64_t umax = cost.empty() ? 0 : *std::max_element(cost.begin(), cost.end());
+    std::fprintf(stderr, "sched: %zu units over %d lists: max/mean load %.4f, largest unit %.4f of mean\n",
+                 cost.size(), G, tot ? double(mx) * G / double(tot) : 0.0, tot ? double(umax) * G / double(tot) : 0.0);
   }
   L.G = G;
   L.host.assign(1, 0);
