@@ -1,4 +1,4 @@
-"""The N>1 host path over real process boundaries (gloo, world size 2, CPU):
+"""The N>1 host path over real process boundaries (gloo, world size 2 and 8, CPU):
 every rank builds its own cad_layer_plan, the row exchanges run as
 torch.distributed all_to_all_single with the plan's per-peer counts, the
 oracle plays the server kernels, and each rank checks its home rows against
@@ -12,8 +12,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-LENGTHS = [900, 50, 70, 180, 200, 136]
-WORLD = 2
+CASES = {2: [900, 50, 70, 180, 200, 136],
+         # 8 ranks (the driver's largest scaling run): a long document over 4 ranks
+         8: [1400, 40, 100, 500, 60, 300, 200, 128, 72]}
 
 
 def _free_port():
@@ -32,7 +33,7 @@ def _a2a(x, rows, shape_tail):
     return out.numpy()
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, WORLD, LENGTHS):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
@@ -105,11 +106,14 @@ def _worker(rank, port, q):
         dist.destroy_process_group()
 
 
-def test_gloo_world2_dispatch_roundtrip():
+@pytest.mark.parametrize("world", sorted(CASES))
+def test_gloo_dispatch_roundtrip(world):
+    WORLD, LENGTHS = world, CASES[world]
+    assert sum(LENGTHS) % WORLD == 0
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, WORLD, LENGTHS)) for r in range(WORLD)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(WORLD))

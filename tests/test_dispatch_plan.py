@@ -16,6 +16,7 @@ SHAPE = CF.Shape("test", 2, 1)
     (2, [700, 60, 120, 400, 256, 512]),          # one long doc straddling devices
     (3, [1500, 30, 90, 70, 100, 130]),           # heavy skew -> splits + migrations
     (4, [300, 300, 300, 300, 300, 300, 300, 300]),
+    (8, [1400, 40, 100, 500, 60, 300, 200, 128, 72]),  # 8 ranks, one document over four
 ])
 def test_distributed_layer_matches_whole_batch(world, lengths):
     total = sum(lengths)
