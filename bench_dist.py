@@ -65,7 +65,10 @@ def run(args, metric, load_peaks, ClockSampler):
         raise ValueError(f"unknown CAD_WORKLOAD {workload!r}")
     per_gpu = total // world
     lengths = S.sample_batch(dist_, total)
-    lp = D.LayerPlan(lengths, world, rank, shape)
+    # ping/pong halves: the reference's assign_halves split (0) or evened out
+    # per server in causal pairs (1, cad_layer_plan_create_ex)
+    balance = os.environ.get("CAD_BALANCE_HALVES", "0") != "0"
+    lp = D.LayerPlan(lengths, world, rank, shape, balance_halves=balance)
     obj = [D.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = D.Comm(obj[0], rank, world)
@@ -97,7 +100,8 @@ def run(args, metric, load_peaks, ClockSampler):
     # layer l+1 and the return of layer l overlap the other half's CA
     layers = int(os.environ.get("CAD_LAYERS", "1" if workload == "cfg4" else "4")) if transport == "ce" else 1
     if transport == "ce":
-        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape) for r in range(world)], o, lse, dq,
+        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape, balance_halves=balance) for r in range(world)],
+                               o, lse, dq,
                                layers=layers, copy_mode=copy_mode, copy_ctas=copy_ctas)
 
     def step(mode="pingpong"):
@@ -226,6 +230,7 @@ def run(args, metric, load_peaks, ClockSampler):
                                    f"ping-pong halves, {layers} stacked CA layer(s) fwd+bwd per step "
                                    "(identity between layers)",
                        "workload_id": workload, "layers_per_step": layers,
+                       "halves": "balanced per server" if balance else "reference assign_halves",
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
                        "parallelism": f"CA servers x{world} (scheduler sharding)",

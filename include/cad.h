@@ -368,6 +368,16 @@ typedef struct cad_xfer {
 int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items,
                           int64_t n_items, int32_t rank, int64_t q_row_bytes,
                           int64_t kv_row_bytes, cad_layer_plan** out);
+/* Same, with balance != 0: each server's halves evened out in causal pairs
+ * (to within 1 %) by moving the query tail of the heavier half's largest
+ * contiguous CA-task into the other half. The reference's halves
+ * (assign_halves, P/src/sim.cpp:34-46) balance nothing per server; served
+ * tasks, residency and results are unchanged, only the ping/pong split
+ * moves. balance = 0 is cad_layer_plan_create. */
+int cad_layer_plan_create_ex(const cad_plan* plan, const cad_item* home_items,
+                             int64_t n_items, int32_t rank, int64_t q_row_bytes,
+                             int64_t kv_row_bytes, int32_t balance,
+                             cad_layer_plan** out);
 int cad_layer_plan_info(const cad_layer_plan* lp, int32_t half,
                         cad_layer_half_info* info);
 int cad_layer_plan_xfer(const cad_layer_plan* lp, int32_t half, int32_t which,

@@ -141,6 +141,7 @@ SIGNATURES = {
     "cad_ca_bwd_parts": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int, vp]),
     "cad_ca_plan_set_max_ctas": (C.c_int, [vp, C.c_int]),
     "cad_layer_plan_create": (C.c_int, [vp, P(cad_item), i64, i32, i64, i64, P(vp)]),
+    "cad_layer_plan_create_ex": (C.c_int, [vp, P(cad_item), i64, i32, i64, i64, i32, P(vp)]),
     "cad_layer_plan_info": (C.c_int, [vp, i32, P(cad_layer_half_info)]),
     "cad_layer_plan_xfer": (C.c_int, [vp, i32, i32, P(cad_xfer)]),
     "cad_layer_plan_destroy": (None, [vp]),

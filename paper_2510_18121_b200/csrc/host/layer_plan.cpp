@@ -27,6 +27,7 @@
 //   OR  O/LSE (and dQ in backward) server -> home  KVR dK/dV server -> owner
 //       (partials of one row from several servers are summed at the owner).
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <memory>
 #include <vector>
@@ -117,6 +118,67 @@ struct Builder {
   }
 };
 
+// One CA-task as served: query positions [qb, qe) of a plan task's document
+// over keys [0, kv) (kv = qe for contiguous items), in half `half`.
+struct Part {
+  i64 task, qb, qe, kv;
+  int half;
+  bool splittable;  // contiguous item part (head_tail parts keep the reference's pairing)
+};
+
+i64 part_pairs(const Part& p) { return cad::causal_pairs(p.qe - p.qb, p.kv); }
+
+// The CA-tasks of server s: the reference's served list and halves
+// (assign_halves, P/src/sim.cpp:34-46) -- and, with `balance`, the halves
+// evened out in causal pairs by moving the query tail of the heavier half's
+// largest contiguous task (a query shard with its causal prefix is itself a
+// CA-task) to the lighter half. The reference balances cores per server but
+// not per half; the halves of one server can differ several-fold (one long
+// document), and every half of every rank waits for its peers' previous
+// returns, so the per-half maximum over ranks sets the step time.
+std::vector<Part> server_parts(const cad::Plan& P, const cad::DevicePlan& dev, bool balance) {
+  std::vector<Part> parts;
+  for (const cad::Served& sv : dev.served) {
+    const cad::Item& it = P.tasks[static_cast<size_t>(sv.task)].item;
+    const bool ht = it.layout == cad::Layout::head_tail;
+    parts.push_back({sv.task, it.q_begin, it.q_end, it.q_end, sv.half, !ht});
+    if (ht) parts.push_back({sv.task, it.ht_mirror - it.q_end, it.ht_mirror - it.q_begin,
+                             it.ht_mirror - it.q_begin, sv.half, false});
+  }
+  if (!balance) return parts;
+  for (int round = 0; round < 4; ++round) {
+    i64 load[2] = {0, 0};
+    for (const Part& p : parts) load[p.half] += part_pairs(p);
+    const int heavy = load[1] > load[0] ? 1 : 0;
+    const i64 delta = (load[heavy] - load[1 - heavy]) / 2;
+    if (delta <= (load[0] + load[1]) / 200) break;  // within 1 %
+    int best = -1;
+    for (size_t i = 0; i < parts.size(); ++i)
+      if (parts[i].half == heavy && parts[i].splittable &&
+          (best < 0 || part_pairs(parts[i]) > part_pairs(parts[static_cast<size_t>(best)])))
+        best = static_cast<int>(i);
+    if (best < 0) break;
+    Part& b = parts[static_cast<size_t>(best)];
+    if (part_pairs(b) <= delta) {
+      b.half = 1 - heavy;
+      continue;
+    }
+    // c with pairs of queries [c, qe) ~ delta: sum_{p=c}^{qe-1} (p+1) =
+    // (qe(qe+1) - c(c+1)) / 2, c rounded to a 128-row tile of the task
+    const double t = double(b.qe) * double(b.qe + 1) - 2.0 * double(delta);
+    i64 c = static_cast<i64>(std::sqrt(std::max(0.0, t)));
+    c = b.qb + (c - b.qb + 64) / 128 * 128;
+    if (c <= b.qb || c >= b.qe) break;
+    Part tail = b;
+    tail.qb = c;
+    tail.half = 1 - heavy;
+    b.qe = c;
+    b.kv = c;
+    parts.push_back(tail);
+  }
+  return parts;
+}
+
 }  // namespace
 
 extern "C" {
@@ -124,6 +186,12 @@ extern "C" {
 int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int64_t n_items,
                           int32_t rank, int64_t q_row_bytes, int64_t kv_row_bytes,
                           cad_layer_plan** out) {
+  return cad_layer_plan_create_ex(plan, home_items, n_items, rank, q_row_bytes, kv_row_bytes, 0, out);
+}
+
+int cad_layer_plan_create_ex(const cad_plan* plan, const cad_item* home_items, int64_t n_items,
+                             int32_t rank, int64_t q_row_bytes, int64_t kv_row_bytes, int32_t balance,
+                             cad_layer_plan** out) {
   return cad::guarded([&] {
     if (!plan || !out || (n_items > 0 && !home_items)) throw cad::DomainError("null argument");
     *out = nullptr;
@@ -152,6 +220,8 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
     L->rank = rank;
     L->world = world;
     L->home_rows = rows_of[static_cast<size_t>(rank)];
+    std::vector<std::vector<Part>> parts_of;
+    for (int32_t s = 0; s < world; ++s) parts_of.push_back(server_parts(P, devs[static_cast<size_t>(s)], balance != 0));
     for (int h = 0; h < 2; ++h) {
       Builder qd(world), kvd(world);
       std::vector<Half> all(static_cast<size_t>(world));  // server-side layouts of every rank
@@ -160,11 +230,10 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
         std::map<i64, std::pair<i64, i64>> group;  // doc -> (kv_off, need)
         std::vector<i64> doc_order;
         // KV need per document over this half's tasks
-        for (const cad::Served& sv : devs[static_cast<size_t>(s)].served) {
-          if (sv.half != h) continue;
-          const cad::Item& it = P.tasks[static_cast<size_t>(sv.task)].item;
-          const i64 need = it.layout == cad::Layout::head_tail ? std::max(it.kv_extent, it.ht_mirror - it.q_begin)
-                                                               : it.kv_extent;
+        for (const Part& pt : parts_of[static_cast<size_t>(s)]) {
+          if (pt.half != h) continue;
+          const cad::Item& it = P.tasks[static_cast<size_t>(pt.task)].item;
+          const i64 need = pt.kv;
           auto g = group.find(it.doc);
           if (g == group.end()) {
             group[it.doc] = {0, need};
@@ -179,33 +248,25 @@ int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items, int6
           kv_off += group[d].second;
         }
         H.kv_rows = kv_off;
-        for (const cad::Served& sv : devs[static_cast<size_t>(s)].served) {
-          if (sv.half != h) continue;
-          const cad::Task& t = P.tasks[static_cast<size_t>(sv.task)];
-          const cad::Item& it = t.item;
-          // (query begin, end) of the CA-tasks of this item: its head, and
-          // for head_tail its mirrored tail; each sees keys [0, end)
-          std::pair<i64, i64> parts[2] = {{it.q_begin, it.q_end}, {0, 0}};
-          int n_parts = 1;
-          if (it.layout == cad::Layout::head_tail) parts[n_parts++] = {it.ht_mirror - it.q_end, it.ht_mirror - it.q_begin};
+        for (const Part& pt : parts_of[static_cast<size_t>(s)]) {
+          if (pt.half != h) continue;
+          const cad::Item& it = P.tasks[static_cast<size_t>(pt.task)].item;
           const auto& segs = owners.at(it.doc);
-          for (int k = 0; k < n_parts; ++k) {
-            const i64 qb = parts[k].first, qe = parts[k].second;
-            cad_ca_task ct;
-            ct.q_off = H.q_rows;
-            ct.n_q = qe - qb;
-            ct.kv_off = group[it.doc].first;
-            ct.kv_len = qe;
-            H.tasks.push_back(ct);
-            H.task_index.push_back(sv.task);
-            // Q rows come from the task's home device
-            for (i64 pos = qb; pos < qe; ++pos) {
-              const Seg& o = owner_of(segs, pos);
-              if (o.device != it.home) throw cad::DomainError("task rows not on its home device");
-              qd.add(o.device, s, o.home_row + (pos - o.begin), H.q_rows + (pos - qb));
-            }
-            H.q_rows += qe - qb;
+          const i64 qb = pt.qb, qe = pt.qe;
+          cad_ca_task ct;
+          ct.q_off = H.q_rows;
+          ct.n_q = qe - qb;
+          ct.kv_off = group[it.doc].first;
+          ct.kv_len = pt.kv;
+          H.tasks.push_back(ct);
+          H.task_index.push_back(pt.task);
+          // Q rows come from the task's home device
+          for (i64 pos = qb; pos < qe; ++pos) {
+            const Seg& o = owner_of(segs, pos);
+            if (o.device != it.home) throw cad::DomainError("task rows not on its home device");
+            qd.add(o.device, s, o.home_row + (pos - o.begin), H.q_rows + (pos - qb));
           }
+          H.q_rows += qe - qb;
         }
         for (i64 d : doc_order) {
           const auto& segs = owners.at(d);

@@ -74,10 +74,13 @@ class LayerPlan:
 
     def __init__(self, lengths: Sequence[int], world: int, rank: int, shape: CF.Shape,
                  cfg: Optional[S.SchedulerConfig] = None, tokens_per_device: Optional[int] = None,
-                 items: Optional[Sequence[S.Item]] = None):
+                 items: Optional[Sequence[S.Item]] = None, balance_halves: bool = False):
         """Home items from place_sequential(lengths) (DistCA's chunks), or the
         given `items` (e.g. head_tail per-document CP shards; a head_tail
-        item's home rows are its head rows, then its tail rows)."""
+        item's home rows are its head rows, then its tail rows).
+        balance_halves: even out each server's ping/pong halves in causal
+        pairs (cad_layer_plan_create_ex) instead of the reference's
+        assign_halves split."""
         total = sum(lengths)
         self.world, self.rank, self.shape = world, rank, shape
         self.tokens_per_device = tokens_per_device or total // world
@@ -90,7 +93,8 @@ class LayerPlan:
         lp = C.c_void_p()
         q_row = shape.h_q * shape.head_dim * 2
         kv_row = 2 * shape.h_kv * shape.head_dim * 2
-        check(lib().cad_layer_plan_create(ph.h, arr, len(self.home_items), rank, q_row, kv_row, C.byref(lp)))
+        check(lib().cad_layer_plan_create_ex(ph.h, arr, len(self.home_items), rank, q_row, kv_row,
+                                             int(balance_halves), C.byref(lp)))
         try:
             self.halves: List[HalfPlan] = []
             for h in (0, 1):

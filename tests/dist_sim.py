@@ -50,12 +50,12 @@ def home_arrays(plans, lengths, per_doc):
     return homes
 
 
-def run_layer(lengths, world, shape, seed=0, items=None):
+def run_layer(lengths, world, shape, seed=0, items=None, balance_halves=False):
     """Returns (home outputs of the distributed run, whole-batch reference),
     both in home layout per rank: dicts of o, lse, dq, dk, dv. `items`:
     explicit home items (default: place_sequential of the lengths)."""
     rng = np.random.default_rng(seed)
-    plans = [D.LayerPlan(lengths, world, r, shape, items=items) for r in range(world)]
+    plans = [D.LayerPlan(lengths, world, r, shape, items=items, balance_halves=balance_halves) for r in range(world)]
     hq, hkv, d = shape.h_q, shape.h_kv, shape.head_dim
     per = {n: [rng.standard_normal((l, h, d), dtype=np.float32) for l in lengths]
            for n, h in (("q", hq), ("k", hkv), ("v", hkv), ("do", hq))}

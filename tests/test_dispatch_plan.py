@@ -18,10 +18,11 @@ SHAPE = CF.Shape("test", 2, 1)
     (4, [300, 300, 300, 300, 300, 300, 300, 300]),
     (8, [1400, 40, 100, 500, 60, 300, 200, 128, 72]),  # 8 ranks, one document over four
 ])
-def test_distributed_layer_matches_whole_batch(world, lengths):
+@pytest.mark.parametrize("balance", [False, True])
+def test_distributed_layer_matches_whole_batch(world, lengths, balance):
     total = sum(lengths)
     assert total % world == 0
-    out, ref, plans = run_layer(lengths, world, SHAPE, seed=world)
+    out, ref, plans = run_layer(lengths, world, SHAPE, seed=world, balance_halves=balance)
     assert plans[0].plan.migrations > 0 or world == 4
     for r in range(world):
         for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
@@ -122,3 +123,23 @@ def test_pp_tick_plan_executes():
         for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
             err = np.abs(out[name][r] - ref[name][r]).max()
             assert err < tol, (r, name, err)
+
+
+def test_balanced_halves_even_out_each_server():
+    """cad_layer_plan_create_ex(balance=1): per server, the two halves carry
+    equal causal pairs to within a tile's worth, the served pairs are those
+    of the reference split, and config 3 at 8 GPUs goes from several-fold
+    half imbalance to ~1."""
+    from paper_2510_18121_b200 import dispatch as D
+    from paper_2510_18121_b200 import scheduler as S
+    lengths = S.sample_batch(CF.length_dist("pretrain", 1), 65536 * 8)
+
+    def pairs(hp):
+        return sum(S.exact_causal_pairs(t.n_q, t.kv_len) for t in hp.tasks)
+
+    for r in range(8):
+        ref = D.LayerPlan(lengths, 8, r, CF.LLAMA8B)
+        bal = D.LayerPlan(lengths, 8, r, CF.LLAMA8B, balance_halves=True)
+        a, b = pairs(bal.halves[0]), pairs(bal.halves[1])
+        assert a + b == pairs(ref.halves[0]) + pairs(ref.halves[1])
+        assert abs(a - b) <= 0.02 * (a + b) + 2 * 128 * 131072, (r, a, b)
