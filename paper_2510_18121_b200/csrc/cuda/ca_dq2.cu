@@ -28,7 +28,7 @@ namespace cad_dev {
 namespace dq2 {
 
 #ifndef CAD_DQ_EMU_MASK
-#define CAD_DQ_EMU_MASK 0
+#define CAD_DQ_EMU_MASK 0x1111  // 25 % of the exp2 pairs on the FMA pipe: measured -1 % (A/B, config 2)
 #endif
 constexpr uint32_t kDqEmuMask = CAD_DQ_EMU_MASK;
 constexpr int kThreads = 384;
