@@ -32,7 +32,13 @@ namespace dq2 {
 #endif
 constexpr uint32_t kDqEmuMask = CAD_DQ_EMU_MASK;
 constexpr int kThreads = 384;
-constexpr int kKStages = 3, kVStages = 2;
+#ifndef CAD_DQ2_KSTAGES
+#define CAD_DQ2_KSTAGES 3
+#endif
+#ifndef CAD_DQ2_VSTAGES
+#define CAD_DQ2_VSTAGES 2
+#endif
+constexpr int kKStages = CAD_DQ2_KSTAGES, kVStages = CAD_DQ2_VSTAGES;
 constexpr uint32_t kHalfBytes = kTileBytes / 2;  // 16 KB
 constexpr uint32_t kQOff = 0;                    // own head: Q, dO (32 KB each)
 constexpr uint32_t kDOOff = kTileBytes;
