@@ -220,9 +220,13 @@ static void deal(CtaLists& L, const std::vector<int64_t>& cost, int G) {
 // Per-unit cost in tile iterations, plus the unit's fixed prologue/epilogue.
 static void build_schedules(cad_ca_plan& P) {
   std::vector<int64_t> c;
+  // fixed per-unit cost in tile iterations (fill/drain, epilogue);
+  // CAD_SCHED_FIXED / CAD_SCHED_KV_FIXED override for experiments
+  static const int64_t fixed_q = std::getenv("CAD_SCHED_FIXED") ? std::atoll(std::getenv("CAD_SCHED_FIXED")) : 1;
+  static const int64_t fixed_kv = std::getenv("CAD_SCHED_KV_FIXED") ? std::atoll(std::getenv("CAD_SCHED_KV_FIXED")) : -1;
   auto fwd_cost = [&](const std::vector<FwdUnit>& v) {
     c.clear();
-    for (const FwdUnit& u : v) c.push_back(int64_t(u.n_kv) + 1);
+    for (const FwdUnit& u : v) c.push_back(int64_t(u.n_kv) + fixed_q);
     return c;
   };
   deal(P.sched_fwd, fwd_cost(P.fwd_units), P.grid(P.fwd_units.size()));
@@ -234,10 +238,11 @@ static void build_schedules(cad_ca_plan& P) {
        std::max<int>(1, std::min<int64_t>(P.dq2_units.size(), P.grid(1 << 30) / 2)));
   c.clear();
   const int group = P.shape.h_q / P.shape.h_kv;
-  for (const KvUnit& u : P.kv_units) c.push_back(int64_t(u.n_iter) + 2 * group);
+  const int64_t kv_fixed = fixed_kv >= 0 ? fixed_kv : 2 * group;
+  for (const KvUnit& u : P.kv_units) c.push_back(int64_t(u.n_iter) + kv_fixed);
   deal(P.sched_kv, c, P.grid(P.kv_units.size()));
   c.clear();
-  for (const KvUnit& u : P.kv2_units) c.push_back(int64_t(u.n_iter) + 2 * group);
+  for (const KvUnit& u : P.kv2_units) c.push_back(int64_t(u.n_iter) + kv_fixed);
   deal(P.sched_kv2, c, std::max<int>(1, std::min<int64_t>(P.kv2_units.size(), P.grid(1 << 30) / 2)));
 }
 
