@@ -33,6 +33,9 @@ namespace fwd2 {
 #endif
 constexpr uint32_t kPairEmuMask = CAD_EMU_MASK;  // 4 of 16 exp2 pairs on the FMA pipe (measured best)
 constexpr int kThreads = 384;
+#ifndef CAD_FWD2_TMA_STORE
+#define CAD_FWD2_TMA_STORE 1
+#endif
 #ifndef CAD_FWD2_STAGES
 #define CAD_FWD2_STAGES 3
 #endif
@@ -41,7 +44,11 @@ constexpr uint32_t kHalfBytes = kTileBytes / 2;           // 16 KB: half a K or 
 constexpr uint32_t kQOff = 0;                             // 2 x 32 KB
 constexpr uint32_t kKOff = 2 * kTileBytes;                // kStages x 16 KB (64 kv rows x 128 d)
 constexpr uint32_t kVOff = kKOff + kStages * kHalfBytes;  // kStages x 16 KB (128 kv rows x 64 d)
-constexpr uint32_t kBarOff = kVOff + kStages * kHalfBytes;
+// O staging per softmax warpgroup (head): 128 rows x 128 d bf16 as two
+// SW128 planes, written out by TMA stores (coalesced, asynchronous); rows
+// of a partial last tile go out with per-thread stores instead.
+constexpr uint32_t kOStOff = kVOff + kStages * kHalfBytes;
+constexpr uint32_t kBarOff = kOStOff + (CAD_FWD2_TMA_STORE ? 2 * kTileBytes : 0);
 constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 
 struct Bars {
@@ -52,7 +59,7 @@ struct Bars {
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_k64, tm_v;  // tm_k64: 64-row boxes
+  CUtensorMap tm_q, tm_k64, tm_v, tm_o;  // tm_k64: 64-row boxes
   const DevTask* tasks;
   const FwdUnit* units;  // nh == 4: heads head0..head0+3
   int n_units;
@@ -257,20 +264,52 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
       const float inv = 1.f / l;
       const int head = un.head0 + 2 * rank + h;
       __nv_bfloat16* orow = p.o + ((int64_t)(tk.q_off + qi) * p.h_q + head) * kHeadDim;
+      const bool full_tile = un.tile * kTile + kTile <= tk.n_q;  // uniform over the warpgroup
+      if (CAD_FWD2_TMA_STORE && full_tile) {
+        // stage the normalised rows in SW128 planes, one TMA store per plane
+        uint8_t* st = smem + kOStOff + h * kTileBytes;
+        if (row == 0) bulk_wait_read0();  // the previous unit's stores have read the staging
+        named_sync(1 + h, 128);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(o_tmem + c * 32, r);
-        tmem_wait_ld();
-        uint4 w[4];
-        uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_tmem + c * 32, r);
+          tmem_wait_ld();
+          uint4 w[4];
+          uint32_t* wp = reinterpret_cast<uint32_t*>(w);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
-        if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+          for (int i = 0; i < 16; ++i)
+            wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+          uint8_t* plane = st + (c >> 1) * (kTileBytes / 2) + row * 128;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = w[i];
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(plane + ((((c & 1) * 4 + i) ^ (row & 7)) << 4)) = w[i];
+        }
+        fence_proxy_async_smem();
+        named_sync(1 + h, 128);
+        if (row == 0) {
+          const int qrow0 = tk.q_off + un.tile * kTile;
+          tma_store_3d(&p.tm_o, st, 0, qrow0, head);
+          tma_store_3d(&p.tm_o, st + kTileBytes / 2, 64, qrow0, head);
+          bulk_commit();
+        }
+      } else {
+        // partial last tile of a task: per-thread stores of the valid rows
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_tmem + c * 32, r);
+          tmem_wait_ld();
+          uint4 w[4];
+          uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = w[i];
+          }
         }
       }
       if (valid) p.lse[(int64_t)head * p.q_rows + tk.q_off + qi] = (m + __log2f(l)) * 0.69314718055994531f;
@@ -279,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
     }
   }
 
+  if (CAD_FWD2_TMA_STORE && warp < 8 && (warp & 3) == 0 && lane == 0) bulk_wait0();  // staging read + stores done
   tc_fence_before();
   cluster_sync_all();
   if (warp == 9) tmem_free_2sm<512>(tmem);
@@ -294,6 +334,7 @@ bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, cons
   make_tile_map(&p.tm_q, q, plan->shape.q_rows, plan->shape.h_q);
   make_tile_map(&p.tm_k64, k, plan->shape.kv_rows, plan->shape.h_kv, 64);
   make_tile_map(&p.tm_v, v, plan->shape.kv_rows, plan->shape.h_kv);
+  make_tile_map(&p.tm_o, o, plan->shape.q_rows, plan->shape.h_q);
   p.tasks = plan->d_tasks;
   p.units = plan->d_fwd2;
   p.n_units = static_cast<int>(plan->fwd2_units.size());
