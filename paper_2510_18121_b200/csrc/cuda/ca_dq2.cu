@@ -46,7 +46,10 @@ constexpr uint32_t kDOOff = kTileBytes;
 constexpr uint32_t kKOff = 2 * kTileBytes;
 constexpr uint32_t kKStageBytes = 2 * kHalfBytes;
 constexpr uint32_t kVOff = kKOff + kKStages * kKStageBytes;  // V stage: K-major 64 kv rows x 128 d
-constexpr uint32_t kBarOff = kVOff + kVStages * kHalfBytes;
+// dQ staging: one 16 KB SW128 plane per element-wise warpgroup (its 64 d
+// columns of the tile), written out by a TMA store for full tiles
+constexpr uint32_t kOStOff = kVOff + kVStages * kHalfBytes;
+constexpr uint32_t kBarOff = kOStOff + kTileBytes;
 constexpr uint32_t kSmemBytes = kBarOff + 256 + 1024;
 static_assert(kSmemBytes <= 232448, "dQ pair shared memory");
 
@@ -66,7 +69,7 @@ struct Ring {
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_do, tm_k64, tm_k, tm_v64;  // *64: 64-row boxes
+  CUtensorMap tm_q, tm_do, tm_k64, tm_k, tm_v64, tm_dq;  // *64: 64-row boxes
   const DevTask* tasks;
   const FwdUnit* units;  // nh == 2: heads head0, head0 + 1
   int n_units;
@@ -324,12 +327,25 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
       mbar_wait_warp(&bars->dq_full, dq_ph);
       dq_ph ^= 1;
       tc_fence_after();
-      tmem_row_to_global(tDQ + lsel + c0, p.scale,
-                         p.dq + (row * p.h_q + head) * kHeadDim + c0, valid);
+      if (all_rows) {
+        uint8_t* st = smem + kOStOff + w * (kTileBytes / 2);
+        if (r == 0) bulk_wait_read0();  // the previous unit's store has read the staging
+        named_sync(1 + w, 128);
+        tmem_row_to_smem_sw128(tDQ + lsel + c0, p.scale, st, r);
+        fence_proxy_async_smem();
+        named_sync(1 + w, 128);
+        if (r == 0) {
+          tma_store_3d(&p.tm_dq, st, c0, tk.q_off + un.tile * kTile, head);
+          bulk_commit();
+        }
+      } else {
+        tmem_row_to_global(tDQ + lsel + c0, p.scale, p.dq + (row * p.h_q + head) * kHeadDim + c0, valid);
+      }
       tc_fence_before();
       mbar_arrive_leader(&bars->dq_free);
     }
   }
+  if (warp < 8 && (warp & 3) == 0 && lane == 0) bulk_wait0();  // dQ staging read + stores done
   tc_fence_before();
   cluster_sync_all();
   if (warp == 9) tmem_free_2sm<512>(tmem);
@@ -348,6 +364,7 @@ bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const
   make_tile_map(&p.tm_k64, k, sh.kv_rows, sh.h_kv, 64);
   make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
   make_tile_map(&p.tm_v64, v, sh.kv_rows, sh.h_kv, 64);
+  make_tile_map(&p.tm_dq, dq, sh.q_rows, sh.h_q);
   p.tasks = plan->d_tasks;
   p.units = plan->d_dq2;
   p.n_units = static_cast<int>(plan->dq2_units.size());

@@ -50,4 +50,23 @@ __device__ __forceinline__ void tmem_row_to_global(uint32_t taddr, float mul, __
   }
 }
 
+// Same 64 columns, scaled, into row `row` of a 128-row x 64-column bf16
+// SW128 plane in shared memory (the layout a 64 x 128-row TMA box stores).
+__device__ __forceinline__ void tmem_row_to_smem_sw128(uint32_t taddr, float mul, uint8_t* plane, uint32_t row) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    uint4 w[4];
+    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * mul, __uint_as_float(r[2 * i + 1]) * mul);
+    uint8_t* line = plane + row * 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) *reinterpret_cast<uint4*>(line + (((c * 4 + i) ^ (row & 7)) << 4)) = w[i];
+  }
+}
+
 }  // namespace cad_dev
