@@ -33,7 +33,13 @@ namespace kv2 {
 #endif
 constexpr uint32_t kDkdvEmuMask = CAD_DKDV_EMU_MASK;
 constexpr int kThreads = 384;
-constexpr int kQStages = 3, kDOStages = 2;
+#ifndef CAD_KV2_QSTAGES
+#define CAD_KV2_QSTAGES 2  // 2 measured 1.5 % faster than 3 at config 2 (A/B) and frees the staging below
+#endif
+#ifndef CAD_KV2_TMA_STORE
+#define CAD_KV2_TMA_STORE 1
+#endif
+constexpr int kQStages = CAD_KV2_QSTAGES, kDOStages = 2;
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
 // Q / dO stage (32 KB): [K-major: q rows 64r..64r+63, two 8 KB d-planes |
@@ -42,7 +48,10 @@ constexpr uint32_t kQOff = 2 * kTileBytes;
 constexpr uint32_t kDOOff = kQOff + kQStages * kTileBytes;
 constexpr uint32_t kLseOff = kDOOff + kDOStages * kTileBytes;
 constexpr uint32_t kDOff = kLseOff + kQStages * 512;
-constexpr uint32_t kBarOff = kDOff + kDOStages * 512;
+// dV/dK staging: one 16 KB SW128 plane per element-wise warpgroup (its 64 d
+// columns), used for dV then dK; full tiles leave by TMA stores
+constexpr uint32_t kStOff = (kDOff + kDOStages * 512 + 1023) / 1024 * 1024;
+constexpr uint32_t kBarOff = CAD_KV2_TMA_STORE ? kStOff + kTileBytes : kDOff + kDOStages * 512;
 constexpr uint32_t kSmemBytes = kBarOff + 256;
 static_assert(kSmemBytes <= 232448, "dK/dV pair shared memory");
 
@@ -64,7 +73,7 @@ struct KRing {
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_q64, tm_k, tm_v, tm_do, tm_do64;
+  CUtensorMap tm_q, tm_q64, tm_k, tm_v, tm_do, tm_do64, tm_dk, tm_dv;
   const float* nlse2;
   const float* ndelta;
   int64_t pitch;
@@ -455,12 +464,40 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_pair_kernel(const __g
       const int row = un.kv_off + kj;
       const bool valid = row < un.kv_end;
       const int64_t off = (int64_t(row) * p.h_kv + un.hk) * kHeadDim + c0;
-      tmem_row_to_global(tDV + lsel + c0, 1.f, p.dv + off, valid);
-      tmem_row_to_global(tDK + lsel + c0, p.scale, p.dk + off, valid);
-      tc_fence_before();
-      mbar_arrive_leader(&bars->acc_free);
+      const int row0 = un.kv_off + (un.tile + int(rank)) * kTile;
+      if (CAD_KV2_TMA_STORE && row0 + kTile <= un.kv_end) {
+        uint8_t* st = smem + kStOff + w * (kTileBytes / 2);
+        if (r == 0) bulk_wait_read0();  // the previous unit's dK store has read the staging
+        named_sync(1 + w, 128);
+        tmem_row_to_smem_sw128(tDV + lsel + c0, 1.f, st, r);
+        uint32_t pk[32];  // dK row, packed, while dV leaves
+        tmem_row_to_regs_bf16(tDK + lsel + c0, p.scale, pk);
+        tc_fence_before();
+        mbar_arrive_leader(&bars->acc_free);  // TMEM read out: the next unit may accumulate
+        fence_proxy_async_smem();
+        named_sync(1 + w, 128);
+        if (r == 0) {
+          tma_store_3d(&p.tm_dv, st, c0, row0, un.hk);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        named_sync(1 + w, 128);
+        regs_to_smem_sw128(pk, st, r);
+        fence_proxy_async_smem();
+        named_sync(1 + w, 128);
+        if (r == 0) {
+          tma_store_3d(&p.tm_dk, st, c0, row0, un.hk);
+          bulk_commit();
+        }
+      } else {
+        tmem_row_to_global(tDV + lsel + c0, 1.f, p.dv + off, valid);
+        tmem_row_to_global(tDK + lsel + c0, p.scale, p.dk + off, valid);
+        tc_fence_before();
+        mbar_arrive_leader(&bars->acc_free);
+      }
     }
   }
+  if (CAD_KV2_TMA_STORE && warp < 8 && (warp & 3) == 0 && lane == 0) bulk_wait0();  // stores done
   tc_fence_before();
   cluster_sync_all();
   if (warp == 9) tmem_free_2sm<512>(tmem);
@@ -481,6 +518,8 @@ bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, con
   make_tile_map(&p.tm_do64, dout, sh.q_rows, sh.h_q, 64);
   make_tile_map(&p.tm_k, k, sh.kv_rows, sh.h_kv);
   make_tile_map(&p.tm_v, v, sh.kv_rows, sh.h_kv);
+  make_tile_map(&p.tm_dk, dk, sh.kv_rows, sh.h_kv);
+  make_tile_map(&p.tm_dv, dv, sh.kv_rows, sh.h_kv);
   p.nlse2 = nlse2;
   p.ndelta = ndelta;
   p.pitch = pitch;

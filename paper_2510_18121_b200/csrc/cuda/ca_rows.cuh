@@ -69,4 +69,25 @@ __device__ __forceinline__ void tmem_row_to_smem_sw128(uint32_t taddr, float mul
   }
 }
 
+// 64 TMEM columns of this thread's row, scaled and packed to bf16x2.
+__device__ __forceinline__ void tmem_row_to_regs_bf16(uint32_t taddr, float mul, uint32_t (&pk)[32]) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      pk[16 * c + i] = pack_bf16(__uint_as_float(r[2 * i]) * mul, __uint_as_float(r[2 * i + 1]) * mul);
+  }
+}
+// 32 packed bf16x2 (64 columns) into row `row` of a SW128 plane.
+__device__ __forceinline__ void regs_to_smem_sw128(const uint32_t (&pk)[32], uint8_t* plane, uint32_t row) {
+  uint8_t* line = plane + row * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<uint4*>(line + ((j ^ (row & 7)) << 4)) =
+        make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+}
+
 }  // namespace cad_dev
