@@ -194,6 +194,10 @@ def run(args, metric, load_peaks, ClockSampler):
         t0 = fw[0][3] if fw else None
         trace = None if t0 is None else sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
                          round(b.elapsed_time(c), 2)) for (k, l, h, a, b, c) in tr], key=lambda r: r[3])
+    traces = None
+    if os.environ.get("CAD_TRACE") and layer.ce is not None:
+        traces = [None] * world
+        dist.all_gather_object(traces, trace)
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_, hdo_)) * world
     d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv)) * world
 
@@ -259,6 +263,10 @@ def run(args, metric, load_peaks, ClockSampler):
             out["trace_rank0"] = {"columns": ["kind", "layer", "half", "t_ms", "flag_wait_ms", "kernel_ms"],
                                   "rows": trace,
                                   "flag_wait_total_ms": round(sum(r[4] for r in trace if r[0] in "FB"), 2)}
+            out["trace_ranks"] = [None if t is None else {
+                "flag_wait_total_ms": round(sum(r[4] for r in t if r[0] in "FB"), 2),
+                "kernel_total_ms": round(sum(r[5] for r in t if r[0] in "FB"), 2),
+                "phases": [(r[0], r[1], r[2], r[4], r[5]) for r in t if r[0] in "FB"]} for t in traces]
         print(json.dumps(out))
     comm.close()
     dist.barrier()
