@@ -39,7 +39,11 @@ constexpr int kThreads = 384;
 #ifndef CAD_KV2_TMA_STORE
 #define CAD_KV2_TMA_STORE 1
 #endif
-constexpr int kQStages = CAD_KV2_QSTAGES, kDOStages = 2;
+#ifndef CAD_KV2_DOSTAGES
+#define CAD_KV2_DOSTAGES 2
+#endif
+constexpr int kQStages = CAD_KV2_QSTAGES, kDOStages = CAD_KV2_DOSTAGES;
+static_assert(kQStages >= 2, "the Q ring needs two stages (S^T(i+1) loads while dK(i) reads Q(i))");
 constexpr uint32_t kKOff = 0;
 constexpr uint32_t kVOff = kTileBytes;
 // Q / dO stage (32 KB): [K-major: q rows 64r..64r+63, two 8 KB d-planes |
