@@ -52,13 +52,6 @@ struct KvSeg {
 // Static per-CTA work lists: CTA (or CTA pair) c runs units
 // list[off[c] .. off[c+1]) in order. Stored on the device as one array:
 // off[0..G] followed by list.
-// A work unit with its task, stored in a CTA's list order (one independent
-// 32-byte load per unit instead of list -> unit -> task).
-struct UnitRec {
-  FwdUnit un;
-  DevTask tk;
-};
-
 struct CtaLists {
   int G = 0;
   std::vector<int32_t> host;  // off (G + 1) then list
@@ -88,7 +81,6 @@ struct cad_ca_plan {
   cad_dev::FwdUnit* d_dq = nullptr;
   cad_dev::FwdUnit* d_fwd2 = nullptr;
   cad_dev::FwdUnit* d_dq2 = nullptr;
-  cad_dev::UnitRec* d_seq_dq2 = nullptr;  // sched_dq2's list as (unit, task) records
   cad_dev::KvUnit* d_kv = nullptr;
   cad_dev::KvUnit* d_kv2 = nullptr;
   cad_dev::KvSeg* d_segs = nullptr;

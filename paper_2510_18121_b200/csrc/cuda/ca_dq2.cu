@@ -72,7 +72,6 @@ struct Params {
   CUtensorMap tm_q, tm_do, tm_k64, tm_k, tm_v64, tm_dq;  // *64: 64-row boxes
   const DevTask* tasks;
   const FwdUnit* units;  // nh == 2: heads head0, head0 + 1
-  const UnitRec* seq;    // the work lists as (unit, task) records, same indexing as sched
   int n_units;
   const int32_t* sched;
   int group;
@@ -162,9 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
       Ring<kKStages> kr;
       Ring<kVStages> vr;
       for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
-        const UnitRec rec = p.seq[ui];
-        const FwdUnit un = rec.un;
-        const DevTask tk = rec.tk;
+        const int u = sched_unit(p.sched, n_pairs, ui);
+        const FwdUnit un = p.units[u];
+        const DevTask tk = p.tasks[un.task];
         const int hk = un.head0 / p.group;
         const int head = un.head0 + int(rank);
         const int qrow = tk.q_off + un.tile * kTile;
@@ -204,7 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
       auto sKm = [&](uint32_t i) { return sbase + kKOff + i * kKStageBytes + kHalfBytes; };
       auto sVk = [&](uint32_t i) { return sbase + kVOff + i * kHalfBytes; };
       for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
-        const int n = p.seq[ui].un.n_kv;
+        const int u = sched_unit(p.sched, n_pairs, ui);
+        const FwdUnit un = p.units[u];
+        const int n = un.n_kv;
         mbar_wait(&bars->q_full, q_it & 1);
         ++q_it;
         const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
@@ -264,31 +265,17 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
     const uint32_t lsel = ((warp & 3) * 32) << 16;
     const int c0 = 64 * w;
     uint32_t s_ph = 0, dp_ph = 0, dq_ph = 0;
-    // The next unit's record and -LSE/-D values are fetched during the
-    // current unit (no dependent global loads at a unit boundary).
-    const int ue = sched_end(p.sched, pair);
-    int ui = sched_begin(p.sched, pair);
-    UnitRec nrec = ui < ue ? p.seq[ui] : UnitRec{};
-    float pf_l2 = 0.f, pf_dd = 0.f;
-    auto row_stats = [&](const UnitRec& rc, float& l2, float& d) {
-      const int q = rc.un.tile * kTile + r;
-      const bool ok = q < rc.tk.n_q;
-      const int64_t rw = int64_t(rc.tk.q_off) + q;
-      const int hd = rc.un.head0 + int(rank);
-      l2 = ok ? -p.lse2[int64_t(hd) * p.pitch + rw] : 0.f;
-      d = ok ? -p.delta[int64_t(hd) * p.pitch + rw] : 0.f;
-    };
-    if (ui < ue) row_stats(nrec, pf_l2, pf_dd);
-    for (; ui < ue; ++ui) {
-      const FwdUnit un = nrec.un;
-      const DevTask tk = nrec.tk;
-      const float lse2 = pf_l2, dd = pf_dd;
-      if (ui + 1 < ue) nrec = p.seq[ui + 1];
+    for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
+      const int u = sched_unit(p.sched, n_pairs, ui);
+      const FwdUnit un = p.units[u];
+      const DevTask tk = p.tasks[un.task];
       const int shift = tk.kv_len - tk.n_q;
       const int qi = un.tile * kTile + r;
       const bool valid = qi < tk.n_q;
       const int64_t row = int64_t(tk.q_off) + qi;
       const int head = un.head0 + int(rank);  // this CTA's query head
+      const float lse2 = valid ? -p.lse2[int64_t(head) * p.pitch + row] : 0.f;
+      const float dd = valid ? -p.delta[int64_t(head) * p.pitch + row] : 0.f;
       const int pos = valid ? shift + qi : -1;  // invalid rows see nothing
       const bool all_rows = un.tile * kTile + kTile <= tk.n_q;
       for (int j = 0; j < un.n_kv; ++j) {
@@ -336,7 +323,6 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive_leader(&bars->ds_full);
-        if (j == 0 && ui + 1 < ue) row_stats(nrec, pf_l2, pf_dd);
       }
       mbar_wait_warp(&bars->dq_full, dq_ph);
       dq_ph ^= 1;
@@ -381,7 +367,6 @@ bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const
   make_tile_map(&p.tm_dq, dq, sh.q_rows, sh.h_q);
   p.tasks = plan->d_tasks;
   p.units = plan->d_dq2;
-  p.seq = plan->d_seq_dq2;
   p.n_units = static_cast<int>(plan->dq2_units.size());
   p.sched = plan->sched_dq2.d;
   p.group = sh.h_q / sh.h_kv;

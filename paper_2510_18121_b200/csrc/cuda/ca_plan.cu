@@ -236,22 +236,6 @@ static void build_schedules(cad_ca_plan& P) {
   deal(P.sched_dq, fwd_cost(P.dq_units), P.grid(P.dq_units.size()));
   deal(P.sched_dq2, fwd_cost(P.dq2_units),
        std::max<int>(1, std::min<int64_t>(P.dq2_units.size(), P.grid(1 << 30) / 2)));
-  {
-    // the dQ pair kernel reads its list as (unit, task) records
-    const CtaLists& L = P.sched_dq2;
-    std::vector<UnitRec> seq;
-    for (size_t k = size_t(L.G) + 1; k < L.host.size(); ++k) {
-      const FwdUnit& u = P.dq2_units[size_t(L.host[k])];
-      seq.push_back({u, P.tasks[size_t(u.task)]});
-    }
-    cudaFree(P.d_seq_dq2);
-    P.d_seq_dq2 = nullptr;
-    const size_t bytes = std::max<size_t>(1, seq.size()) * sizeof(UnitRec);
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&P.d_seq_dq2), bytes), "cudaMalloc(seq)");
-    if (!seq.empty())
-      cuda_check(cudaMemcpy(P.d_seq_dq2, seq.data(), seq.size() * sizeof(UnitRec), cudaMemcpyHostToDevice),
-                 "cudaMemcpy(seq)");
-  }
   c.clear();
   const int group = P.shape.h_q / P.shape.h_kv;
   const int64_t kv_fixed = fixed_kv >= 0 ? fixed_kv : 2 * group;
@@ -352,7 +336,6 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     cudaFree(plan->d_dq);
     cudaFree(plan->d_fwd2);
     cudaFree(plan->d_dq2);
-    cudaFree(plan->d_seq_dq2);
     cudaFree(plan->d_kv);
     cudaFree(plan->d_kv2);
     cudaFree(plan->d_segs);
