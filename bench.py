@@ -42,7 +42,7 @@ def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return pk["bf16_tflops"], pk.get("bf16_tflops_sustained"), "measured"
+        return pk["bf16_tflops"], pk.get("bf16_tflops_sustained") or pk["bf16_tflops"], "measured"
     except Exception:
         return 1590.0, 1400.0, "fallback"
 
