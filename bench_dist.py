@@ -194,6 +194,38 @@ def run(args, metric, load_peaks, ClockSampler):
         t0 = fw[0][3] if fw else None
         trace = None if t0 is None else sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
                          round(b.elapsed_time(c), 2)) for (k, l, h, a, b, c) in tr], key=lambda r: r[3])
+    # NVLink probe: one half's forward dispatch (Q + K/V rows this rank pushes
+    # into its peers' buffers) alone on a stream, own rows on another stream;
+    # achieved GB/s = remote bytes / time of the pushes, per rank
+    probe = None
+    if layer.ce is not None:
+        ce = layer.ce
+        ps, loc = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        saved = ce.local_stream
+        ce.local_stream = loc
+        q_row, kv_row = shape.h_q * 128 * 2, shape.h_kv * 128 * 2
+        best = []
+        for h in (0, 1):
+            nbytes = lp.halves[h].remote_send_bytes[0] + lp.halves[h].remote_send_bytes[1]
+            ms_h = []
+            for _ in range(3):
+                dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(ps)
+                ce._copy(h, D.XFER_Q, q.data_ptr(), f"q{h}_0", q_row, ps)
+                ce._copy(h, D.XFER_KV, k.data_ptr(), f"k{h}_0", kv_row, ps)
+                ce._copy(h, D.XFER_KV, v.data_ptr(), f"v{h}_0", kv_row, ps)
+                e1.record(ps)
+                torch.cuda.synchronize()
+                ms_h.append(e0.elapsed_time(e1))
+            best.append((nbytes, min(ms_h)))
+        ce.local_stream = saved
+        dist.barrier()
+        probe = best
+    probes = [None] * world
+    dist.all_gather_object(probes, probe)
+
     traces = None
     if os.environ.get("CAD_TRACE") and layer.ce is not None:
         traces = [None] * world
@@ -249,6 +281,12 @@ def run(args, metric, load_peaks, ClockSampler):
                      "ms_pingpong": ms, "hidden_fraction": hidden,
                      "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
                      "nvlink_gbs_per_gpu": float(allst[:, 2].max()) / (ms_comm / 1e3) / 1e9 if ms_comm else None,
+                     # per rank and half: a forward dispatch pushed alone (copy engines, peer
+                     # memory over NVLink), remote bytes / time, against 900 GB/s per direction
+                     "nvlink_probe_gbs": None if probes[0] is None else [
+                         [round(b / (t / 1e3) / 1e9, 1) if t > 0 and b > 0 else None for (b, t) in pr] for pr in probes],
+                     "nvlink_probe_bytes": None if probes[0] is None else [[b for (b, t) in pr] for pr in probes],
+                     "nvlink_link_gbs": 900.0,
                      "ref_total_comm_bytes": lp.plan.total_comm_bytes},
             "roofline": {"kernel": "ca fwd+bwd (4 launches per half)", "bound": "tensor",
                          "achieved": flops / world / ms_compute / 1e9, "peak": peak, "unit": "TFLOP/s",
