@@ -4,16 +4,17 @@ Workload: BASELINE config 3 shape (Llama-3-8B CA, 32 Q / 8 KV heads), 65536
 tokens per GPU (512K at 8 GPUs), pretrain_upsampled documents (seed 1),
 placed sequentially; CA-tasks sharded by the bit-exact scheduler; per layer
 the Q/KV dispatch, CA fwd, O/LSE return, dO dispatch, CA bwd, dQ and dK/dV
-return run with ping/pong halves (dispatch.py) over copy-engine pushes
-(CUDA IPC, default; CAD_TRANSPORT=nccl for NCCL all-to-allv). A step is
-CAD_LAYERS (default 4) stacked CA layers, forward then backward, with the
-identity between layers, so transfers of one layer overlap the neighbouring
-layer's CA compute. Scaling is weak (fixed tokens per GPU). Times are CUDA
-events on the compute stream, max over ranks.
+return run with ping/pong halves through the C-ABI executor (cad_layer_ctx,
+one cad_layer_step call per step): CUDA-IPC copy-engine pushes with GPU
+flags (default) and, in the same run, the NCCL all-to-allv transport. A step
+is CAD_LAYERS (default 4) stacked CA layers, forward then backward, with the
+identity between layers (benchmark mode: dK/dV summed over the layers), so
+the transfers of one layer overlap the neighbouring layer's CA compute.
+Scaling is weak (fixed tokens per GPU). Times are CUDA events on the compute
+stream, max over ranks.
 """
 import json
 import os
-import statistics
 
 import torch
 import torch.distributed as dist
@@ -52,7 +53,6 @@ def run(args, metric, load_peaks, ClockSampler):
     # CAD_WORKLOAD: cfg3 (default; 8B, 64K tokens per GPU, weak scaling),
     # cfg4 (34B, 64 Q / 8 KV heads, 1M tokens over the N GPUs: strong
     # scaling, docs up to 256K) or cfg5-<uniform|lognormal|prolong|fixed>
-    # (the imbalance sweep's distributions at the config-3 shape)
     workload = os.environ.get("CAD_WORKLOAD", "cfg3")
     seed = int(os.environ.get("CAD_SEED", "1"))
     if workload == "cfg4":
@@ -65,22 +65,11 @@ def run(args, metric, load_peaks, ClockSampler):
         raise ValueError(f"unknown CAD_WORKLOAD {workload!r}")
     per_gpu = total // world
     lengths = S.sample_batch(dist_, total)
-    # ping/pong halves: the reference's assign_halves split (0) or evened out
-    # per server in causal pairs (1, cad_layer_plan_create_ex)
     balance = os.environ.get("CAD_BALANCE_HALVES", "0") != "0"
     lp = D.LayerPlan(lengths, world, rank, shape, balance_halves=balance)
-    obj = [D.Comm.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    comm = D.Comm(obj[0], rank, world)
-    transport = os.environ.get("CAD_TRANSPORT", "ce")
-    # copy-engine transport: row pushes by copy engines ('ce') or by an SM
-    # copy kernel on CAD_COPY_CTAS SMs kept free of CA work ('sm')
-    copy_mode = os.environ.get("CAD_COPY", "ce")
-    copy_ctas = int(os.environ.get("CAD_COPY_CTAS", "4"))
-    reserve = int(os.environ.get("CAD_RESERVE_SMS", (str(copy_ctas) if copy_mode == "sm" else "0")
-                                 if transport == "ce" else "8"))
+    layers = int(os.environ.get("CAD_LAYERS", "1" if workload == "cfg4" else "4"))
     dev = torch.device("cuda", local)
-    layer = D.DistCALayer(lp, comm, dev, reserve_sms=reserve)
+    layer = D.DistCALayer(lp, dev, "ipc", layers=layers, balance_halves=balance, bench_stacked=layers > 1)
     H = lp.home_rows
     g = torch.Generator(device=dev).manual_seed(rank)
     bf = dict(device=dev, dtype=torch.bfloat16)
@@ -91,53 +80,66 @@ def run(args, metric, load_peaks, ClockSampler):
     o = torch.empty_like(q)
     lse = torch.empty(shape.h_q, H, device=dev)
     dq = torch.empty_like(q)
-    dk_acc = torch.zeros(H, shape.h_kv, 128, device=dev)
-    dv_acc = torch.zeros_like(dk_acc)
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)
+    layer.bind_outputs(o, lse, dq)
+    layer.connect_dist()
+    io = layer.io(q, k, v, do, o, lse, dq, dk, dv)
     comp = torch.cuda.current_stream(dev)
-    # stacked CA layers per step (copy-engine transport): the dispatch of
-    # layer l+1 and the return of layer l overlap the other half's CA
-    layers = int(os.environ.get("CAD_LAYERS", "1" if workload == "cfg4" else "4")) if transport == "ce" else 1
-    if transport == "ce":
-        layer.use_copy_engines([D.LayerPlan(lengths, world, r, shape, balance_halves=balance) for r in range(world)],
-                               o, lse, dq,
-                               layers=layers, copy_mode=copy_mode, copy_ctas=copy_ctas)
 
-    def step(mode="pingpong"):
-        layer.step(q, k, v, do, o, lse, dq, dk_acc, dv_acc, mode=mode)
-        lib = D.lib()
-        lib.cad_f32_to_bf16(dk_acc.data_ptr(), dk_acc.numel(), dk.data_ptr(), comp.cuda_stream)
-        lib.cad_f32_to_bf16(dv_acc.data_ptr(), dv_acc.numel(), dv.data_ptr(), comp.cuda_stream)
+    def step(L=layer, mode="pingpong", io_=None):
+        L.step(io_ or io, mode, comp)
 
     for _ in range(args.warmup):
         step()
-    layer.launches = 0
-    if layer.ce is not None:
-        layer.ce.launches = 0
+    l0 = layer.launches
     clocks = ClockSampler(local)
     clocks.start()
     ms, my_ms = _timed(step, args.steps, comp)
     clk = clocks.stop()
-    launches = layer.launches + (layer.ce.launches if layer.ce is not None else 0) + 2 * args.steps
-    ms_compute, my_compute = _timed(lambda: step("compute"), max(2, args.steps // 2), comp)
-    ms_comm, _ = _timed(lambda: step("comm"), max(2, args.steps // 2), comp)
-    ms_serial = None
-    if transport != "ce":
-        ms_serial, _ = _timed(lambda: step("serial"), max(2, args.steps // 2), comp)  # NCCL, no overlap
-    ms_signal = None
-    if layer.ce is not None:
-        ms_signal, _ = _timed(lambda: step("signal"), max(2, args.steps // 2), comp)
+    launches = layer.launches - l0
+    n_side = max(2, args.steps // 2)
+    ms_compute, my_compute = _timed(lambda: step(mode="compute"), n_side, comp)
+    ms_comm, _ = _timed(lambda: step(mode="comm"), n_side, comp)
+    ms_signal, _ = _timed(lambda: step(mode="signal"), n_side, comp)
+    ms_serial, _ = _timed(lambda: step(mode="serial"), n_side, comp)
 
-    # e2e: home inputs from pinned host memory, gradients back to host,
-    # double-buffered as in bench.py: step j's inputs go host -> device on a
-    # copy stream while step j-1 runs, step j's gradients come back while
-    # step j+1 runs. dq is written by the peers' pushes (fixed, IPC-exported
-    # buffer), so it is first staged device-side on the compute stream.
+    # NCCL transport (north_star's all-to-allv on a side stream), same
+    # schedule and layers, CA grid leaving CAD_NCCL_RESERVE SMs to NCCL
+    nccl = None
+    if os.environ.get("CAD_NCCL_LINE", "1") != "0":
+        reserve = int(os.environ.get("CAD_NCCL_RESERVE", "8"))
+        obj = [D.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = D.Comm(obj[0], rank, world)
+        ln = D.DistCALayer(lp, dev, "nccl", layers=layers, reserve_sms=reserve, balance_halves=balance,
+                           bench_stacked=layers > 1)
+        ln.set_comm(comm)
+        for _ in range(2):
+            step(ln)
+        n_ms, _ = _timed(lambda: step(ln), max(3, args.steps // 2), comp)
+        n_comp, _ = _timed(lambda: step(ln, "compute"), n_side, comp)
+        n_comm, _ = _timed(lambda: step(ln, "comm"), n_side, comp)
+        n_serial, _ = _timed(lambda: step(ln, "serial"), n_side, comp)
+        ln.close()
+        comm.close()
+        nccl = {"ms_pingpong": n_ms, "ms_compute_only": n_comp, "ms_comm_only": n_comm, "ms_serial": n_serial,
+                "reserve_sms": reserve,
+                "hidden_fraction": max(0.0, min(1.0, 1.0 - (n_ms - n_comp) / n_comm)) if n_comm > 0 else None}
+
+    # e2e: home inputs from pinned host memory, O/LSE/dQ/dK/dV back to host,
+    # double-buffered: step j's inputs go host -> device on a copy stream
+    # while step j-1 runs, step j's outputs come back while step j+1 runs.
+    # o/lse/dq are written by the peers' pushes (bound, IPC-exported
+    # buffers), so they are first staged device-side on the compute stream.
     hq_, hk_, hv_, hdo_ = (t.cpu().pin_memory() for t in (q, k, v, do))
-    hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (dq, dk, dv))
-    sets = [(q, k, v, do, dk, dv, torch.empty_like(dq)),
-            tuple(torch.empty_like(t) for t in (q, k, v, do, dk, dv, dq))]
+    outs = (o, lse, dq, dk, dv)
+    host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in outs]
+    sets = []
+    for j in range(2):
+        ins = (q, k, v, do) if j == 0 else tuple(torch.empty_like(t) for t in (q, k, v, do))
+        stage = tuple(torch.empty_like(t) for t in outs)
+        sets.append((ins, stage, layer.io(*ins, o, lse, dq, stage[3], stage[4])))
     copy = torch.cuda.Stream(device=dev)
 
     def e2e_run(n):
@@ -149,28 +151,25 @@ def run(args, metric, load_peaks, ClockSampler):
         st.record(copy)
         for j in range(n + 1):
             if j < n:  # inputs of step j
-                b = sets[j % 2]
+                ins, _, _ = sets[j % 2]
                 if comp_done[j % 2] is not None:
                     copy.wait_event(comp_done[j % 2])
                 with torch.cuda.stream(copy):
-                    for dst, src in zip(b[:4], (hq_, hk_, hv_, hdo_)):
+                    for dst, src in zip(ins, (hq_, hk_, hv_, hdo_)):
                         dst.copy_(src, non_blocking=True)
                 h2d_done[j % 2] = ev()
                 h2d_done[j % 2].record(copy)
-            if j >= 1:  # results of step j-1
+            if j >= 1:  # outputs of step j-1
                 with torch.cuda.stream(copy):
                     copy.wait_event(comp_done[(j - 1) % 2])
-                    b = sets[(j - 1) % 2]
-                    for dst, src in zip((hdq, hdk, hdv), (b[6], b[4], b[5])):
+                    for dst, src in zip(host_out, sets[(j - 1) % 2][1]):
                         dst.copy_(src, non_blocking=True)
             if j < n:  # step j
-                b = sets[j % 2]
+                _, stage, io_j = sets[j % 2]
                 comp.wait_event(h2d_done[j % 2])
-                layer.step(b[0], b[1], b[2], b[3], o, lse, dq, dk_acc, dv_acc)
-                lib = D.lib()
-                lib.cad_f32_to_bf16(dk_acc.data_ptr(), dk_acc.numel(), b[4].data_ptr(), comp.cuda_stream)
-                lib.cad_f32_to_bf16(dv_acc.data_ptr(), dv_acc.numel(), b[5].data_ptr(), comp.cuda_stream)
-                b[6].copy_(dq, non_blocking=True)
+                step(io_=io_j)
+                for dst, src in zip(stage[:3], (o, lse, dq)):
+                    dst.copy_(src, non_blocking=True)
                 comp_done[j % 2] = ev()
                 comp_done[j % 2].record(comp)
         en.record(copy)
@@ -182,60 +181,34 @@ def run(args, metric, load_peaks, ClockSampler):
 
     e2e_run(2)
     ms_e2e = e2e_run(max(3, args.steps))
-    trace = None
-    if os.environ.get("CAD_TRACE") and layer.ce is not None:
-        # per-kernel flag waits on the compute stream in one ping-pong step
-        layer.ce.trace = []
-        step(os.environ.get("CAD_TRACE_MODE", "pingpong"))
-        torch.cuda.synchronize()
-        tr = layer.ce.trace
-        layer.ce.trace = None
-        fw = [x for x in tr if x[0] == "F"]
-        t0 = fw[0][3] if fw else None
-        trace = None if t0 is None else sorted([(k, l, h, round(t0.elapsed_time(a), 2), round(a.elapsed_time(b), 2),
-                         round(b.elapsed_time(c), 2)) for (k, l, h, a, b, c) in tr], key=lambda r: r[3])
+
     # NVLink probe: one half's forward dispatch (Q + K/V rows this rank pushes
     # into its peers' buffers) alone on a stream, own rows on another stream;
     # achieved GB/s = remote bytes / time of the pushes, per rank
-    probe = None
-    if layer.ce is not None:
-        ce = layer.ce
-        ps, loc = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        saved = ce.local_stream
-        ce.local_stream = loc
-        q_row, kv_row = shape.h_q * 128 * 2, shape.h_kv * 128 * 2
-        best = []
-        for h in (0, 1):
-            nbytes = lp.halves[h].remote_send_bytes[0] + lp.halves[h].remote_send_bytes[1]
-            ms_h = []
-            for _ in range(3):
-                dist.barrier()
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(ps)
-                ce._copy(h, D.XFER_Q, q.data_ptr(), f"q{h}_0", q_row, ps)
-                ce._copy(h, D.XFER_KV, k.data_ptr(), f"k{h}_0", kv_row, ps)
-                ce._copy(h, D.XFER_KV, v.data_ptr(), f"v{h}_0", kv_row, ps)
-                e1.record(ps)
-                torch.cuda.synchronize()
-                ms_h.append(e0.elapsed_time(e1))
-            best.append((nbytes, min(ms_h)))
-        ce.local_stream = saved
-        dist.barrier()
-        probe = best
+    ps, loc = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    probe = []
+    for h in (0, 1):
+        nbytes = layer.wire_bytes[h][0] + 2 * layer.wire_bytes[h][1]
+        ms_h = []
+        for _ in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ps)
+            layer.dispatch(0, h, D.DISPATCH_QKV, io, ps, loc)
+            e1.record(ps)
+            torch.cuda.synchronize()
+            ms_h.append(e0.elapsed_time(e1))
+        probe.append((nbytes, min(ms_h)))
+    dist.barrier()
     probes = [None] * world
     dist.all_gather_object(probes, probe)
 
-    traces = None
-    if os.environ.get("CAD_TRACE") and layer.ce is not None:
-        traces = [None] * world
-        dist.all_gather_object(traces, trace)
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_, hdo_)) * world
-    d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv)) * world
-
-    pairs = lp.server_pairs()
-    wire = sum(sum(hp.remote_send_bytes) for hp in lp.halves) * layers
-    wire_fwd = sum(hp.remote_send_bytes[0] * 2 + hp.remote_send_bytes[1] for hp in lp.halves)
+    d2h = sum(t.numel() * t.element_size() for t in host_out) * world
+    pairs = layer.served_pairs
+    wire = sum(layer.wire_bytes[h][0] * 2 + layer.wire_bytes[h][1] * 2 + layer.wire_bytes[h][2] * 2
+               + layer.wire_bytes[h][3] * 2 for h in (0, 1)) * layers
     stats = torch.tensor([pairs, my_compute, wire, my_ms], dtype=torch.float64, device=dev)
     allst = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(allst, stats)
@@ -247,10 +220,8 @@ def run(args, metric, load_peaks, ClockSampler):
         value = flops / ms / 1e9
         # hidden = 1 - (T_pingpong - T_signal) / T_comm_only (the
         # reference's signal/ping-pong modes, P/tests/acceptance.cpp:272-290)
-        hidden = None
-        base = ms_signal if ms_signal is not None else ms_compute
-        if ms_comm > 0:
-            hidden = max(0.0, min(1.0, 1.0 - (ms - base) / ms_comm))
+        hidden = max(0.0, min(1.0, 1.0 - (ms - ms_signal) / ms_comm)) if ms_comm > 0 else None
+        hidden_vs_compute = max(0.0, min(1.0, 1.0 - (ms - ms_compute) / ms_comm)) if ms_comm > 0 else None
         naive_pairs = []
         for r in range(world):
             its = [it for it in lp.home_items if it.home_device == r]
@@ -262,30 +233,30 @@ def run(args, metric, load_peaks, ClockSampler):
             "config": {"workload": f"{_WORKLOADS[workload.split('-')[0]]}: {shape.name} CA ({shape.h_q} Q / {shape.h_kv} KV), "
                                    f"{per_gpu} tokens per GPU ({total} total), "
                                    f"{'pretrain_upsampled' if workload in ('cfg3', 'cfg4') else workload[5:]} lengths seed {seed}, scheduler-sharded, "
-                                   f"{'copy-engine (CUDA IPC) pushes' if transport == 'ce' else 'NCCL all-to-allv'} dispatch/return, "
+                                   "copy-engine (CUDA IPC) pushes through cad_layer_step, "
                                    f"ping-pong halves, {layers} stacked CA layer(s) fwd+bwd per step "
                                    "(identity between layers)",
                        "workload_id": workload, "layers_per_step": layers,
                        "halves": "balanced per server" if balance else "reference assign_halves",
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
-                       "parallelism": f"CA servers x{world} (scheduler sharding)",
-                       "transport": transport, "copy_mode": copy_mode if transport == "ce" else None,
-                       "reserve_sms_for_comm": reserve},
+                       "parallelism": f"CA servers x{world} (scheduler sharding)", "transport": "ipc"},
             "per_gpu_tflops": value / world, "pct_bf16_peak": value / world / peak,
             "tokens_per_s": per_gpu * world * layers / (ms / 1e3),  # token-layers (fwd+bwd) per second
             "imbalance": {"max_over_mean_pairs": float(allst[:, 0].max() / allst[:, 0].mean()),
                           "max_over_mean_ca_time": float(allst[:, 1].max() / allst[:, 1].mean()),
                           "naive_max_over_mean_pairs": max(naive_pairs) / (sum(naive_pairs) / world)},
-            "comm": {"ms_compute_only": ms_compute, "ms_signal": ms_signal, "ms_comm_only": ms_comm, "ms_serial_nccl": ms_serial,
-                     "ms_pingpong": ms, "hidden_fraction": hidden,
+            "comm": {"ms_compute_only": ms_compute, "ms_signal": ms_signal, "ms_comm_only": ms_comm,
+                     "ms_serial": ms_serial, "ms_pingpong": ms, "hidden_fraction": hidden,
+                     "hidden_fraction_vs_compute_only": hidden_vs_compute,
+                     "nccl": nccl,
                      "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
                      "nvlink_gbs_per_gpu": float(allst[:, 2].max()) / (ms_comm / 1e3) / 1e9 if ms_comm else None,
                      # per rank and half: a forward dispatch pushed alone (copy engines, peer
                      # memory over NVLink), remote bytes / time, against 900 GB/s per direction
-                     "nvlink_probe_gbs": None if probes[0] is None else [
-                         [round(b / (t / 1e3) / 1e9, 1) if t > 0 and b > 0 else None for (b, t) in pr] for pr in probes],
-                     "nvlink_probe_bytes": None if probes[0] is None else [[b for (b, t) in pr] for pr in probes],
+                     "nvlink_probe_gbs": [[round(b / (t / 1e3) / 1e9, 1) if t > 0 and b > 0 else None
+                                           for (b, t) in pr] for pr in probes],
+                     "nvlink_probe_bytes": [[b for (b, t) in pr] for pr in probes],
                      "nvlink_link_gbs": 900.0,
                      "ref_total_comm_bytes": lp.plan.total_comm_bytes},
             "roofline": {"kernel": "ca fwd+bwd (4 launches per half)", "bound": "tensor",
@@ -297,15 +268,7 @@ def run(args, metric, load_peaks, ClockSampler):
             "gpu_launches": launches,
             "clocks": clk,
         }
-        if trace is not None:
-            out["trace_rank0"] = {"columns": ["kind", "layer", "half", "t_ms", "flag_wait_ms", "kernel_ms"],
-                                  "rows": trace,
-                                  "flag_wait_total_ms": round(sum(r[4] for r in trace if r[0] in "FB"), 2)}
-            out["trace_ranks"] = [None if t is None else {
-                "flag_wait_total_ms": round(sum(r[4] for r in t if r[0] in "FB"), 2),
-                "kernel_total_ms": round(sum(r[5] for r in t if r[0] in "FB"), 2),
-                "phases": [(r[0], r[1], r[2], r[4], r[5]) for r in t if r[0] in "FB"]} for t in traces]
         print(json.dumps(out))
-    comm.close()
+    layer.close()
     dist.barrier()
     dist.destroy_process_group()

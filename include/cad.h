@@ -458,6 +458,134 @@ int cad_alltoallv(cad_comm* comm, const void* send, const int64_t* send_bytes,
                   const int64_t* recv_bytes, const int64_t* recv_displ,
                   void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* Device: the per-layer executor -- "run this device's layer: dispatch, CA, */
+/* return" (the real counterpart of simulate_layer_pingpong / layer_windows, */
+/* P/include/cadsim/sim.hpp:88, P/src/sim.cpp:69-125,176-221)               */
+/* ---------------------------------------------------------------------- */
+
+/* How rows move between ranks. */
+#define CAD_TRANSPORT_LOCAL 0 /* every rank's context lives in this process
+                                 (one GPU, or GPUs with peer access): peers'
+                                 buffers are addressed directly; the same
+                                 copy/flag code path as IPC */
+#define CAD_TRANSPORT_IPC 1   /* one process per GPU: each rank pushes its
+                                 rows into the peers' buffers (CUDA IPC
+                                 mappings, copy engines) and signals arrival
+                                 with GPU-side flags; no host synchronisation */
+#define CAD_TRANSPORT_NCCL 2  /* gather -> grouped ncclSend/ncclRecv
+                                 all-to-allv -> scatter on the caller's stream */
+
+typedef struct cad_layer_cfg {
+  int32_t rank;
+  int32_t world;
+  int32_t h_q;
+  int32_t h_kv;
+  int32_t head_dim;      /* 128 */
+  float softmax_scale;   /* <= 0: 1/sqrt(head_dim) */
+  int32_t transport;     /* CAD_TRANSPORT_* */
+  int32_t layers;        /* server activation sets. 1 = one CA layer. L > 1 is
+                            a benchmark mode: L stacked CA layers per step with
+                            the identity between them (every layer sees the
+                            step's inputs; O/LSE/dQ are the last layer's, dK/dV
+                            the SUM over the L layers) */
+  int32_t balance_halves; /* 0: the reference's assign_halves split */
+  int32_t reserve_sms;   /* CA kernels leave this many SMs free (NCCL) */
+  int32_t pad_[2];
+} cad_layer_cfg;
+
+typedef struct cad_layer_ctx cad_layer_ctx;
+
+typedef struct cad_layer_ctx_info {
+  int64_t home_rows;          /* rows of this rank's home buffers */
+  int64_t q_rows[2];          /* server Q rows per half */
+  int64_t kv_rows[2];         /* server K/V rows per half */
+  int64_t n_tasks[2];         /* CA-tasks served per half */
+  int64_t served_pairs;       /* exact causal pairs this rank computes */
+  int64_t wire_bytes[2][4];   /* bytes this rank puts on the wire per half and
+                                 CAD_XFER_* of one layer (remote peers only;
+                                 Q/KV count one tensor: x2 for K+V / Q+dO) */
+  int64_t blob_bytes;         /* size of cad_layer_ctx_export's blob */
+  int64_t launches;           /* kernels this context launched so far */
+} cad_layer_ctx_info;
+
+/* Caller buffers of one step on this rank's HOME rows (packed THD, the row
+ * order of the rank's home items): inputs q/dout [home_rows][h_q][d], k/v
+ * [home_rows][h_kv][d] bf16; outputs o/dq bf16 and lse [h_q][home_rows] fp32
+ * (these three must be the buffers given to cad_layer_ctx_bind_outputs),
+ * dk/dv bf16 (may be NULL) and their fp32 sums dk_acc/dv_acc
+ * [home_rows][h_kv][d] (NULL: context-owned). */
+typedef struct cad_layer_io {
+  const void* q;
+  const void* k;
+  const void* v;
+  const void* dout;
+  void* o;
+  float* lse;
+  void* dq;
+  void* dk;
+  void* dv;
+  float* dk_acc;
+  float* dv_acc;
+} cad_layer_io;
+
+/* Builds every rank's row plan (deterministic; cad_layer_plan_create_ex for
+ * each rank), the server CA plans of both halves and the server buffers on
+ * the current device. */
+int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items,
+                         int64_t n_items, const cad_layer_cfg* cfg,
+                         cad_layer_ctx** out);
+int cad_layer_ctx_info_get(const cad_layer_ctx* ctx, cad_layer_ctx_info* info);
+/* Home output buffers the peers write O/LSE/dQ into (before export). */
+int cad_layer_ctx_bind_outputs(cad_layer_ctx* ctx, void* o, float* lse, void* dq);
+/* LOCAL/IPC: this rank's buffer references (blob of info.blob_bytes). Gather
+ * every rank's blob (any host collective), then connect with the
+ * concatenation in rank order. */
+int cad_layer_ctx_export(cad_layer_ctx* ctx, void* blob, size_t cap, size_t* need);
+int cad_layer_ctx_connect(cad_layer_ctx* ctx, const void* blobs, size_t blob_bytes);
+/* NCCL: the communicator of this rank (not owned). */
+int cad_layer_ctx_set_comm(cad_layer_ctx* ctx, cad_comm* comm);
+int cad_layer_ctx_destroy(cad_layer_ctx* ctx);
+
+/* The per-layer entry points (cad_dispatch / cad_return).
+ * A step is: cad_layer_begin, then in dependency order per (layer, half)
+ * dispatch(QKV) -> compute(fwd) -> return(O), dispatch(DO) ->
+ * compute(bwd) -> return(GRAD), then cad_layer_finish. Cross-rank ordering
+ * is the context's job (GPU flags for LOCAL/IPC, the collective for NCCL);
+ * ordering between the caller's streams on one rank is the caller's
+ * (cad_layer_step does both). NCCL: every transport call of one context must
+ * go to one stream. */
+#define CAD_DISPATCH_QKV 0 /* Q, K, V rows: home -> servers (forward)  */
+#define CAD_DISPATCH_DO 1  /* dO rows: home -> servers (backward)      */
+#define CAD_RETURN_O 0     /* O rows + LSE: servers -> home            */
+#define CAD_RETURN_GRAD 1  /* dQ rows -> home, dK/dV partials -> owners */
+int cad_layer_begin(cad_layer_ctx* ctx, void* stream);
+int cad_dispatch(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
+                 const cad_layer_io* io, void* stream);
+/* Same, with this rank's own rows (tasks it serves itself) copied on
+ * local_stream (LOCAL/IPC; cad_layer_step puts them on the compute stream). */
+int cad_dispatch_ex(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
+                    const cad_layer_io* io, void* stream, void* local_stream);
+int cad_layer_compute(cad_layer_ctx* ctx, int32_t layer, int32_t half,
+                      int32_t backward, void* stream);
+int cad_return(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
+               const cad_layer_io* io, void* stream);
+/* Waits for every return addressed to this rank, sums the dK/dV partials into
+ * dk_acc/dv_acc (fp32, zeroed first), writes dk/dv (bf16) if given. */
+int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
+
+/* One whole step (all layers, forward + backward) on `stream` (compute) and
+ * the context's comm stream, in the reference's ping-pong windows. */
+#define CAD_STEP_PINGPONG 0 /* comm of one half under CA of the other */
+#define CAD_STEP_SERIAL 1   /* everything on `stream`, no overlap */
+#define CAD_STEP_COMPUTE 2  /* CA kernels only (server buffers as resident) */
+#define CAD_STEP_COMM 3     /* exchanges only, no CA kernels */
+#define CAD_STEP_SIGNAL 4   /* ping-pong with every flag but no row copies
+                               (the reference's signal mode, sim.hpp:14-18;
+                               LOCAL/IPC only) */
+int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode,
+                   void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -104,6 +104,24 @@ class cad_run(C.Structure):
     _fields_ = [("src_row", i64), ("dst_row", i64), ("n_rows", i64)]
 
 
+class cad_layer_cfg(C.Structure):
+    _fields_ = [("rank", i32), ("world", i32), ("h_q", i32), ("h_kv", i32), ("head_dim", i32),
+                ("softmax_scale", f32), ("transport", i32), ("layers", i32), ("balance_halves", i32),
+                ("reserve_sms", i32), ("pad_", i32 * 2)]
+
+
+class cad_layer_ctx_info(C.Structure):
+    _fields_ = [("home_rows", i64), ("q_rows", i64 * 2), ("kv_rows", i64 * 2), ("n_tasks", i64 * 2),
+                ("served_pairs", i64), ("wire_bytes", (i64 * 4) * 2), ("blob_bytes", i64),
+                ("launches", i64)]
+
+
+class cad_layer_io(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("k", C.c_void_p), ("v", C.c_void_p), ("dout", C.c_void_p),
+                ("o", C.c_void_p), ("lse", C.c_void_p), ("dq", C.c_void_p), ("dk", C.c_void_p),
+                ("dv", C.c_void_p), ("dk_acc", C.c_void_p), ("dv_acc", C.c_void_p)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 
@@ -163,6 +181,20 @@ SIGNATURES = {
     "cad_gather_rows": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "cad_scatter_rows": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "cad_alltoallv": (C.c_int, [vp, vp, P(i64), P(i64), vp, P(i64), P(i64), vp]),
+    "cad_layer_ctx_create": (C.c_int, [vp, P(cad_item), i64, P(cad_layer_cfg), P(vp)]),
+    "cad_layer_ctx_info_get": (C.c_int, [vp, P(cad_layer_ctx_info)]),
+    "cad_layer_ctx_bind_outputs": (C.c_int, [vp, vp, vp, vp]),
+    "cad_layer_ctx_export": (C.c_int, [vp, vp, C.c_size_t, P(C.c_size_t)]),
+    "cad_layer_ctx_connect": (C.c_int, [vp, vp, C.c_size_t]),
+    "cad_layer_ctx_set_comm": (C.c_int, [vp, vp]),
+    "cad_layer_ctx_destroy": (C.c_int, [vp]),
+    "cad_layer_begin": (C.c_int, [vp, vp]),
+    "cad_dispatch": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp]),
+    "cad_dispatch_ex": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp, vp]),
+    "cad_layer_compute": (C.c_int, [vp, i32, i32, i32, vp]),
+    "cad_return": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp]),
+    "cad_layer_finish": (C.c_int, [vp, P(cad_layer_io), vp]),
+    "cad_layer_step": (C.c_int, [vp, P(cad_layer_io), i32, vp]),
 }
 
 _lib = None

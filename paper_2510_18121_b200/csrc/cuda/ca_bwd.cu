@@ -806,16 +806,9 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
     static const bool debug_sync = std::getenv("CAD_DEBUG_SYNC") != nullptr;
     float* delta = static_cast<float*>(workspace);
     float* lse2 = delta + pitch * sh.h_q;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cuda_check(cudaFuncSetAttribute(kv::ca_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kv::kSmemBytes),
-                 "cudaFuncSetAttribute(dkdv)");
-      cuda_check(cudaFuncSetAttribute(dq::ca_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      dq::kSmemBytes),
-                 "cudaFuncSetAttribute(dq)");
-      attr_set = true;
-    }
+    DeviceGuard dg(plan->device);
+    set_max_smem(reinterpret_cast<const void*>(kv::ca_bwd_dkdv_kernel), kv::kSmemBytes, "cudaFuncSetAttribute(dkdv)");
+    set_max_smem(reinterpret_cast<const void*>(dq::ca_bwd_dq_kernel), dq::kSmemBytes, "cudaFuncSetAttribute(dq)");
     // 1. D = rowsum(dO * O)
     if ((parts & CAD_BWD_DELTA) && !plan->row_chunks.empty()) {
       ca_delta_kernel<<<static_cast<unsigned>(plan->row_chunks.size()), kDeltaThreads, sh.h_q * 32 * 4, s>>>(

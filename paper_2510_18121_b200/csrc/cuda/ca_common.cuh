@@ -105,6 +105,19 @@ void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, 
 // 2-D map over a [heads][rows] fp32 buffer (LSE, D): box of 128 rows x 1 head.
 void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
 void cuda_check(cudaError_t e, const char* what);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the current device's context, so a process that
+// drives several GPUs through the C-ABI needs it on each of them. Thread-safe.
+void set_max_smem(const void* kernel, int bytes, const char* what);
+// Makes the plan's device current for the duration of a launch (and restores
+// the caller's device), so one host thread may drive plans on several GPUs.
+struct DeviceGuard {
+  int prev = -1, want = -1;
+  explicit DeviceGuard(int device);
+  ~DeviceGuard();
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
                      cudaStream_t stream);
 bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,

@@ -538,13 +538,8 @@ bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, con
   p.dv = static_cast<__nv_bfloat16*>(dv);
   p.scale = sh.softmax_scale;
   p.scale_log2 = sh.softmax_scale * 1.4426950408889634f;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cuda_check(cudaFuncSetAttribute(kv2::ca_bwd_dkdv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kv2::kSmemBytes),
+  set_max_smem(reinterpret_cast<const void*>(kv2::ca_bwd_dkdv_pair_kernel), kv2::kSmemBytes,
                "cudaFuncSetAttribute(dkdv2)");
-    attr_set = true;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * plan->sched_kv2.G);
   cfg.blockDim = dim3(kv2::kThreads);

@@ -377,13 +377,8 @@ bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const
   p.pitch = pitch;
   p.scale = sh.softmax_scale;
   p.scale_log2 = sh.softmax_scale * 1.4426950408889634f;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cuda_check(cudaFuncSetAttribute(dq2::ca_bwd_dq_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dq2::kSmemBytes),
+  set_max_smem(reinterpret_cast<const void*>(dq2::ca_bwd_dq_pair_kernel), dq2::kSmemBytes,
                "cudaFuncSetAttribute(dq2)");
-    attr_set = true;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * plan->sched_dq2.G);
   cfg.blockDim = dim3(dq2::kThreads);

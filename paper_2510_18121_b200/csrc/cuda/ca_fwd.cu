@@ -282,6 +282,7 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
   return cad::guarded([&] {
     if (!plan || !q || !k || !v || !o || !lse) throw cad::DomainError("null argument");
     if (plan->fwd_units.empty()) return;
+    DeviceGuard dg(plan->device);
     static const bool pair_off = std::getenv("CAD_FWD_PAIR") && std::getenv("CAD_FWD_PAIR")[0] == '0';
     if (!pair_off && launch_fwd_pair(plan, q, k, v, o, lse, static_cast<cudaStream_t>(stream))) return;
     fwd::Params p;
@@ -298,13 +299,7 @@ extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k,
     p.lse = lse;
     p.q_rows = plan->shape.q_rows;
     p.scale_log2 = plan->shape.softmax_scale * 1.4426950408889634f;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cuda_check(cudaFuncSetAttribute(fwd::ca_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      fwd::kSmemBytes),
-                 "cudaFuncSetAttribute(fwd)");
-      attr_set = true;
-    }
+    set_max_smem(reinterpret_cast<const void*>(fwd::ca_fwd_kernel), fwd::kSmemBytes, "cudaFuncSetAttribute(fwd)");
     const int grid = plan->sched_fwd.G;
     fwd::ca_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(p);
     cuda_check(cudaGetLastError(), "ca_fwd launch");

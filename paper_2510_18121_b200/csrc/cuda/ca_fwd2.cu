@@ -345,13 +345,8 @@ bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, cons
   p.lse = lse;
   p.q_rows = plan->shape.q_rows;
   p.scale_log2 = plan->shape.softmax_scale * 1.4426950408889634f;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cuda_check(cudaFuncSetAttribute(fwd2::ca_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    fwd2::kSmemBytes),
+  set_max_smem(reinterpret_cast<const void*>(fwd2::ca_fwd_pair_kernel), fwd2::kSmemBytes,
                "cudaFuncSetAttribute(fwd2)");
-    attr_set = true;
-  }
   const int pairs = plan->sched_fwd2.G;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <queue>
+#include <set>
 #include <string>
 
 #include "../host/cad_status.hpp"
@@ -34,6 +35,31 @@ namespace cad_dev {
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw cad::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void set_max_smem(const void* kernel, int bytes, const char* what) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  const std::pair<const void*, int> key{kernel, dev};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(key)) return;
+  }
+  // idempotent, so a race between two threads only sets it twice
+  cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), what);
+  std::lock_guard<std::mutex> g(mu);
+  done.insert(key);
+}
+
+DeviceGuard::DeviceGuard(int device) : want(device) {
+  cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+  if (prev != want) cuda_check(cudaSetDevice(want), "cudaSetDevice");
+}
+
+DeviceGuard::~DeviceGuard() {
+  if (prev >= 0 && prev != want) cudaSetDevice(prev);
 }
 
 namespace {
@@ -322,6 +348,7 @@ int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info) {
 int cad_ca_plan_set_max_ctas(cad_ca_plan* plan, int max_ctas) {
   return cad::guarded([&] {
     if (!plan || max_ctas < 0) throw cad::DomainError("bad argument");
+    cad_dev::DeviceGuard dg(plan->device);
     plan->max_ctas = max_ctas;
     cad_dev::build_schedules(*plan);
   });
@@ -330,6 +357,7 @@ int cad_ca_plan_set_max_ctas(cad_ca_plan* plan, int max_ctas) {
 int cad_ca_plan_destroy(cad_ca_plan* plan) {
   return cad::guarded([&] {
     if (!plan) return;
+    cad_dev::DeviceGuard dg(plan->device);
     cudaFree(plan->d_tasks);
     cudaFree(plan->d_row_chunks);
     cudaFree(plan->d_fwd);

@@ -40,10 +40,15 @@ struct Nccl {
 
 const Nccl& nccl() {
   static Nccl n;
+  static std::string load_error;
   static std::once_flag once;
   std::call_once(once, [] {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
+    if (!h) {
+      const char* e = dlerror();  // read once: a second call returns NULL
+      load_error = e ? e : "dlopen failed";
+      return;
+    }
     n.h = h;
     n.get_id = reinterpret_cast<decltype(n.get_id)>(dlsym(h, "ncclGetUniqueId"));
     n.init_rank = reinterpret_cast<decltype(n.init_rank)>(dlsym(h, "ncclCommInitRank"));
@@ -54,13 +59,17 @@ const Nccl& nccl() {
     n.recv = reinterpret_cast<decltype(n.recv)>(dlsym(h, "ncclRecv"));
     n.err = reinterpret_cast<decltype(n.err)>(dlsym(h, "ncclGetErrorString"));
   });
-  if (!n.h || !n.get_id || !n.init_rank || !n.send || !n.recv)
-    throw cad::NcclError(std::string("libnccl.so.2 unavailable: ") + (dlerror() ? dlerror() : "?"));
+  if (!n.h) throw cad::NcclError("libnccl.so.2 unavailable: " + load_error);
+  if (!n.get_id || !n.init_rank || !n.destroy || !n.group_start || !n.group_end || !n.send || !n.recv)
+    throw cad::NcclError("libnccl.so.2 lacks a required symbol");
   return n;
 }
 
 void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw cad::NcclError(std::string(what) + ": " + nccl().err(r));
+  if (r == ncclSuccess) return;
+  const Nccl& n = nccl();
+  const char* msg = n.err ? n.err(r) : nullptr;
+  throw cad::NcclError(std::string(what) + ": " + (msg ? msg : ("ncclResult " + std::to_string(int(r)))));
 }
 
 // ------------------------------------------------------------------ kernels
@@ -477,13 +486,8 @@ int cad_copy_spans(const cad_span* spans, int64_t n, int32_t n_ctas, void* strea
     if (simt) {
       cad_dev::copy_spans_kernel<<<n_ctas, 512, 0, static_cast<cudaStream_t>(stream)>>>(spans, n);
     } else {
-      static bool attr = false;
-      if (!attr) {
-        cad_dev::cuda_check(cudaFuncSetAttribute(cad_dev::copy_spans_bulk_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, cad_dev::kBulkSmem),
+      cad_dev::set_max_smem(reinterpret_cast<const void*>(cad_dev::copy_spans_bulk_kernel), cad_dev::kBulkSmem,
                             "cudaFuncSetAttribute(copy_spans_bulk)");
-        attr = true;
-      }
       cad_dev::copy_spans_bulk_kernel<<<n_ctas, 256, cad_dev::kBulkSmem, static_cast<cudaStream_t>(stream)>>>(
           spans, n);
     }

@@ -1,0 +1,844 @@
+// The per-layer executor behind cad_layer_ctx: "run this device's layer --
+// dispatch, CA, return". The reference only models this step
+// (simulate_layer_pingpong over the four windows of layer_windows,
+// P/src/sim.cpp:69-125,176-221; per-device served/sent lists and halves,
+// P/src/sim.cpp:34-46,129-157). Here it moves real rows and runs the sm_100a
+// CA kernels.
+//
+// Per layer and half h of rank r (row lists from cad_layer_plan, built for
+// every rank so each rank knows where its rows land in the peers' buffers):
+//   dispatch QKV   Q rows home -> server, K/V rows owner -> server
+//   compute fwd    cad_ca_fwd on the half's server buffers
+//   return O       O rows + LSE columns server -> home
+//   dispatch DO    dO rows home -> server
+//   compute bwd    cad_ca_bwd (Q/K/V/O/LSE resident from the forward)
+//   return GRAD    dQ rows server -> home, dK/dV partial rows server ->
+//                  the owner's staging; finish sums the partials (fp32)
+//
+// Transports:
+//   LOCAL/IPC  every rank PUSHES its rows straight into the peers' buffers
+//              (cudaMemcpyAsync runs through CUDA IPC mappings: copy
+//              engines, no SM taken from the persistent CA kernels) and
+//              signals arrival with cuStreamWriteValue32 on the peer's flag
+//              word; consumers wait with cuStreamWaitValue32. Nothing
+//              synchronises on the host. LOCAL is the same code with every
+//              rank's context in one process (raw pointers instead of IPC
+//              mappings), which lets one GPU run a world-W layer.
+//   NCCL       gather -> grouped ncclSend/ncclRecv -> scatter, on the stream
+//              the transport call is given.
+// Flag words (uint32, monotonically increasing within a context): slot
+// (kind, half, source rank); the values of one step with L layers starting at
+// g0: forward of layer l -> g0+1+l, backward of layer l -> g0+2L-l, done ->
+// g0+2L, so every wait is ">= value" and a later signal never under-shoots.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/cad_status.hpp"
+#include "ca_common.cuh"
+
+namespace {
+
+using i64 = int64_t;
+using cad_dev::cuda_check;
+
+constexpr int kXQ = CAD_XFER_Q, kXKV = CAD_XFER_KV, kXO = CAD_XFER_O_RET, kXKR = CAD_XFER_KV_RET;
+enum FlagKind { F_QKV = 0, F_DO = 1, F_O = 2, F_G = 3, F_DONE = 4, kKinds = 5 };
+constexpr uint32_t kBlobMagic = 0xCAD1A7E5u;
+
+void ok(int rc, const char* what) {
+  if (rc == CAD_OK) return;
+  const std::string msg = std::string(what) + ": " + cad_last_error();
+  switch (rc) {
+    case CAD_ERR_CONFIG: throw cad::ConfigError(msg);
+    case CAD_ERR_DOMAIN: throw cad::DomainError(msg);
+    case CAD_ERR_NCCL: throw cad::NcclError(msg);
+    case CAD_ERR_CAPACITY: throw cad::CapacityError(msg);
+    default: throw cad::CudaError(msg);
+  }
+}
+
+struct XferRows {
+  std::vector<i64> send_counts, send_idx, recv_counts, recv_idx;
+  i64 n_send() const { return send_idx.size(); }
+  i64 n_recv() const { return recv_idx.size(); }
+};
+
+struct HalfRows {
+  i64 q_rows = 0, kv_rows = 0;
+  std::vector<cad_ca_task> tasks;
+  XferRows x[4];
+  i64 wire[4] = {0, 0, 0, 0};
+};
+
+struct RankRows {
+  i64 home_rows = 0;
+  HalfRows half[2];
+};
+
+RankRows read_rank(const cad_plan* plan, const cad_item* items, i64 n, int32_t rank, i64 q_row, i64 kv_row,
+                   int32_t balance) {
+  cad_layer_plan* lp = nullptr;
+  ok(cad_layer_plan_create_ex(plan, items, n, rank, q_row, kv_row, balance, &lp), "cad_layer_plan_create_ex");
+  std::unique_ptr<cad_layer_plan, void (*)(cad_layer_plan*)> guard(lp, cad_layer_plan_destroy);
+  RankRows R;
+  for (int h = 0; h < 2; ++h) {
+    cad_layer_half_info info;
+    ok(cad_layer_plan_info(lp, h, &info), "cad_layer_plan_info");
+    R.home_rows = info.home_rows;
+    HalfRows& H = R.half[h];
+    H.q_rows = info.q_rows;
+    H.kv_rows = info.kv_rows;
+    H.tasks.assign(info.tasks, info.tasks + info.n_tasks);
+    for (int w = 0; w < 4; ++w) {
+      cad_xfer x;
+      ok(cad_layer_plan_xfer(lp, h, w, &x), "cad_layer_plan_xfer");
+      XferRows& X = H.x[w];
+      X.send_counts.assign(x.send_counts, x.send_counts + x.n_peers);
+      X.recv_counts.assign(x.recv_counts, x.recv_counts + x.n_peers);
+      X.send_idx.assign(x.send_idx, x.send_idx + x.n_send);
+      X.recv_idx.assign(x.recv_idx, x.recv_idx + x.n_recv);
+      H.wire[w] = info.remote_send_bytes[w];
+    }
+  }
+  return R;
+}
+
+// Byte offsets of one rank's context-owned device buffers (one allocation,
+// so IPC exports a single handle). Every rank computes every peer's layout
+// from the peer's row plan.
+struct Bufs {
+  size_t q, k, v, o, dout, dq, dk, dv, lse, sdk, sdv;
+};
+struct Layout {
+  size_t flags = 0;
+  std::vector<std::array<Bufs, 2>> b;  // [layer][half]
+  size_t total = 0;
+};
+
+Layout layout_of(const RankRows& R, int layers, int world, i64 q_row, i64 kv_row, i64 lse_row) {
+  Layout L;
+  size_t off = 0;
+  auto take = [&](i64 bytes) {
+    const size_t at = off;
+    off += (static_cast<size_t>(std::max<i64>(bytes, 16)) + 255) / 256 * 256;
+    return at;
+  };
+  L.flags = take(static_cast<i64>(4) * 2 * kKinds * world);
+  L.b.resize(static_cast<size_t>(layers));
+  for (int l = 0; l < layers; ++l)
+    for (int h = 0; h < 2; ++h) {
+      const HalfRows& H = R.half[h];
+      const i64 qr = std::max<i64>(1, H.q_rows), kr = std::max<i64>(1, H.kv_rows);
+      const i64 sr = std::max<i64>(1, H.x[kXKR].n_recv());
+      Bufs& B = L.b[static_cast<size_t>(l)][static_cast<size_t>(h)];
+      B.q = take(qr * q_row);
+      B.o = take(qr * q_row);
+      B.dout = take(qr * q_row);
+      B.dq = take(qr * q_row);
+      B.k = take(kr * kv_row);
+      B.v = take(kr * kv_row);
+      B.dk = take(kr * kv_row);
+      B.dv = take(kr * kv_row);
+      B.lse = take(qr * lse_row);
+      B.sdk = take(sr * kv_row);
+      B.sdv = take(sr * kv_row);
+    }
+  L.total = off;
+  return L;
+}
+
+// Maximal runs in which both the source and the destination row advance by one.
+std::vector<cad_run> make_runs(const i64* src, const i64* dst, i64 n) {
+  std::vector<cad_run> out;
+  for (i64 i = 0; i < n;) {
+    i64 j = i + 1;
+    while (j < n && src[j] == src[j - 1] + 1 && dst[j] == dst[j - 1] + 1) ++j;
+    out.push_back({src[i], dst[i], j - i});
+    i = j;
+  }
+  return out;
+}
+
+struct BlobRef {
+  uint8_t handle[64];
+  int64_t offset;
+  uint64_t raw;
+};
+struct Blob {
+  uint32_t magic;
+  int32_t rank, world, transport, layers, pad;
+  int64_t home_rows;
+  BlobRef ref[4];  // arena, o, lse, dq
+};
+
+struct Peer {
+  char* arena = nullptr;
+  void* o = nullptr;
+  float* lse = nullptr;
+  void* dq = nullptr;
+  i64 home_rows = 0;
+  Layout layout;
+};
+
+template <class T>
+T* dev_copy(const std::vector<T>& v) {
+  T* d = nullptr;
+  cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), std::max<size_t>(1, v.size()) * sizeof(T)), "cudaMalloc");
+  if (!v.empty()) cuda_check(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy");
+  return d;
+}
+
+}  // namespace
+
+struct cad_layer_ctx {
+  cad_layer_cfg cfg{};
+  int device = 0;
+  int W = 1, me = 0, NL = 1;
+  i64 hq = 0, hkv = 0, d = 128;
+  i64 q_row = 0, kv_row = 0, lse_row = 0;
+  RankRows mine;  // this rank's row plan
+  cad_ca_plan* plan[2] = {nullptr, nullptr};
+  void* ws[2] = {nullptr, nullptr};
+  size_t ws_bytes[2] = {0, 0};
+  i64 pairs = 0;
+  Layout layout;
+  char* arena = nullptr;
+  int32_t* flags = nullptr;
+  std::vector<Peer> peer;
+  std::vector<void*> opened;  // IPC mappings to close
+  std::vector<cad_run> runs[2][4];  // per (half, xfer): runs of all peers, grouped by peer
+  std::vector<size_t> run_off[2][4];  // per peer: first run (W + 1 entries)
+  i64* d_send_idx[2][4] = {};
+  i64* d_recv_idx[2][4] = {};
+  float* acc_own[2] = {nullptr, nullptr};  // dK/dV fp32 sums when the caller gives none
+  void* o_home = nullptr;
+  float* lse_home = nullptr;
+  void* dq_home = nullptr;
+  bool connected = false;
+  cad_comm* comm = nullptr;
+  void* xsend = nullptr;
+  void* xrecv = nullptr;
+  size_t xbytes = 0;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev;
+  uint32_t gen = 0, g0 = 0;
+  i64 launches = 0;
+  bool move = true;  // false: signal mode (flags without row copies)
+
+  // ------------------------------------------------------------- helpers
+  Bufs b(int l, int h) const { return layout.b[static_cast<size_t>(l)][static_cast<size_t>(h)]; }
+  template <class T = void>
+  T* at(size_t off) const { return reinterpret_cast<T*>(arena + off); }
+  template <class T = void>
+  T* peer_at(int p, size_t off) const { return reinterpret_cast<T*>(peer[static_cast<size_t>(p)].arena + off); }
+  const Bufs& pb(int p, int l, int h) const {
+    return peer[static_cast<size_t>(p)].layout.b[static_cast<size_t>(l)][static_cast<size_t>(h)];
+  }
+  uint32_t gl(int l) const { return g0 + 1 + static_cast<uint32_t>(l); }
+  uint32_t gb(int l) const { return g0 + 2 * static_cast<uint32_t>(NL) - static_cast<uint32_t>(l); }
+  uint32_t gdone() const { return g0 + 2 * static_cast<uint32_t>(NL); }
+  bool flagged() const { return cfg.transport != CAD_TRANSPORT_NCCL; }
+  int32_t* flag_of(int p, int kind, int h, int src) const {
+    int32_t* base = p == me ? flags : peer_at<int32_t>(p, peer[static_cast<size_t>(p)].layout.flags);
+    return base + (kind * 2 + h) * W + src;
+  }
+  void signal(int kind, int h, uint32_t value, cudaStream_t s) const {
+    for (int p = 0; p < W; ++p) ok(cad_stream_write_u32(flag_of(p, kind, h, me), value, s), "signal");
+  }
+  void await(int kind, int h, uint32_t value, cudaStream_t s) const {
+    for (int src = 0; src < W; ++src) ok(cad_stream_wait_u32(flag_of(me, kind, h, src), value, s), "await");
+  }
+  cudaEvent_t event(int slot) const { return ev[static_cast<size_t>(slot)]; }
+
+  // rows of exchange x (half h) from src into every peer's buffer dst_of(p);
+  // this rank's own rows go on `local` (the compute stream in a step: a
+  // local copy overlapping a CA kernel crawls and would hold up the remote
+  // pushes queued behind it)
+  template <class DstOf>
+  void push(int h, int x, const void* src, i64 row_bytes, DstOf dst_of, cudaStream_t s, cudaStream_t local) const {
+    if (!move) return;
+    for (int p = 0; p < W; ++p) {
+      const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
+      if (a == e) continue;
+      ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes,
+                       p == me ? local : s),
+         "cad_copy_runs");
+    }
+  }
+  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) const {
+    if (!move) return;
+    for (int p = 0; p < W; ++p) {
+      const size_t a = run_off[h][kXO][static_cast<size_t>(p)], e = run_off[h][kXO][static_cast<size_t>(p) + 1];
+      if (a == e) continue;
+      const Peer& P = peer[static_cast<size_t>(p)];
+      ok(cad_copy_runs_cols(runs[h][kXO].data() + a, static_cast<i64>(e - a), src, src_rows, P.lse, P.home_rows,
+                            static_cast<int32_t>(hq), p == me ? local : s),
+         "cad_copy_runs_cols");
+    }
+  }
+
+  // NCCL: gather, all-to-allv, then scatter (or, with dst_contig, receive
+  // straight into a buffer in recv order)
+  void nccl_rows(int h, int x, const void* src, i64 row_bytes, void* dst, bool dst_contig, cudaStream_t s) {
+    const XferRows& X = mine.half[h].x[x];
+    ok(cad_gather_rows(src, d_send_idx[h][x], X.n_send(), row_bytes, xsend, s), "cad_gather_rows");
+    launches += X.n_send() > 0;
+    alltoallv(X, row_bytes, dst_contig ? dst : xrecv, s);
+    if (!dst_contig) {
+      ok(cad_scatter_rows(xrecv, d_recv_idx[h][x], X.n_recv(), row_bytes, dst, s), "cad_scatter_rows");
+      launches += X.n_recv() > 0;
+    }
+  }
+  void nccl_lse(int h, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s) {
+    const XferRows& X = mine.half[h].x[kXO];
+    ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), d_send_idx[h][kXO], X.n_send(),
+                           static_cast<float*>(xsend), s),
+       "cad_gather_cols_f32");
+    alltoallv(X, lse_row, xrecv, s);
+    ok(cad_scatter_cols_f32(static_cast<const float*>(xrecv), d_recv_idx[h][kXO], X.n_recv(),
+                            static_cast<int32_t>(hq), dst, dst_rows, s),
+       "cad_scatter_cols_f32");
+    launches += (X.n_send() > 0) + (X.n_recv() > 0);
+  }
+  void alltoallv(const XferRows& X, i64 row_bytes, void* recv, cudaStream_t s) const {
+    if (!comm) throw cad::ConfigError("NCCL transport: cad_layer_ctx_set_comm was not called");
+    std::vector<i64> sb(static_cast<size_t>(W)), sd(static_cast<size_t>(W)), rb(static_cast<size_t>(W)),
+        rd(static_cast<size_t>(W));
+    i64 so = 0, ro = 0;
+    for (int p = 0; p < W; ++p) {
+      sb[static_cast<size_t>(p)] = X.send_counts[static_cast<size_t>(p)] * row_bytes;
+      rb[static_cast<size_t>(p)] = X.recv_counts[static_cast<size_t>(p)] * row_bytes;
+      sd[static_cast<size_t>(p)] = so;
+      rd[static_cast<size_t>(p)] = ro;
+      so += sb[static_cast<size_t>(p)];
+      ro += rb[static_cast<size_t>(p)];
+    }
+    ok(cad_alltoallv(comm, xsend, sb.data(), sd.data(), recv, rb.data(), rd.data(), s), "cad_alltoallv");
+  }
+
+  void check_io(const cad_layer_io* io, bool outputs) const {
+    if (!io) throw cad::DomainError("null io");
+    if (outputs && flagged() && (io->o != o_home || io->lse != lse_home || io->dq != dq_home))
+      throw cad::DomainError("o/lse/dq must be the buffers bound with cad_layer_ctx_bind_outputs");
+  }
+  void need_ready() const {
+    if (flagged() && !connected) throw cad::ConfigError("layer context not connected (cad_layer_ctx_connect)");
+    if (!flagged() && !comm) throw cad::ConfigError("NCCL transport: cad_layer_ctx_set_comm was not called");
+  }
+  void check_lh(int l, int h) const {
+    if (l < 0 || l >= NL || h < 0 || h > 1) throw cad::DomainError("layer or half out of range");
+  }
+
+  // ------------------------------------------------------------- phases
+  void begin(cudaStream_t s) {
+    need_ready();
+    g0 = gen;
+    gen += 2 * static_cast<uint32_t>(NL);
+    // every peer finished the previous step: its server buffers are free
+    if (flagged()) await(F_DONE, 0, g0, s);
+  }
+
+  void dispatch(int l, int h, int what, const cad_layer_io* io, cudaStream_t s, cudaStream_t local) {
+    const Bufs& B = b(l, h);
+    if (what == CAD_DISPATCH_QKV) {
+      if (!io->q || !io->k || !io->v) throw cad::DomainError("null q/k/v");
+      if (flagged()) {
+        // identity between stacked layers: layer l's Q/K/V of half h leave
+        // home once every server has returned O(h, l-1)
+        if (l > 0) await(F_O, h, gl(l - 1), s);
+        push(h, kXQ, io->q, q_row, [&](int p) { return peer_at(p, pb(p, l, h).q); }, s, local);
+        push(h, kXKV, io->k, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).k); }, s, local);
+        push(h, kXKV, io->v, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).v); }, s, local);
+        signal(F_QKV, h, gl(l), s);
+      } else if (move) {
+        nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s);
+        nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s);
+        nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s);
+      }
+    } else if (what == CAD_DISPATCH_DO) {
+      if (!io->dout) throw cad::DomainError("null dout");
+      if (flagged()) {
+        if (l < NL - 1) await(F_G, h, gb(l + 1), s);  // dQ(h, l+1) home -> dO(h, l)
+        push(h, kXQ, io->dout, q_row, [&](int p) { return peer_at(p, pb(p, l, h).dout); }, s, local);
+        signal(F_DO, h, gb(l), s);
+      } else if (move) {
+        nccl_rows(h, kXQ, io->dout, q_row, at(B.dout), false, s);
+      }
+    } else {
+      throw cad::DomainError("unknown dispatch kind");
+    }
+  }
+
+  void compute(int l, int h, bool bwd, cudaStream_t s, bool wait_flags, bool run) {
+    if (wait_flags && flagged()) await(bwd ? F_DO : F_QKV, h, bwd ? gb(l) : gl(l), s);
+    if (!run || !plan[h]) return;
+    const Bufs& B = b(l, h);
+    if (!bwd) {
+      ok(cad_ca_fwd(plan[h], at(B.q), at(B.k), at(B.v), at(B.o), at<float>(B.lse), s), "cad_ca_fwd");
+      launches += 1;
+    } else {
+      const size_t kvb = static_cast<size_t>(std::max<i64>(1, mine.half[h].kv_rows) * kv_row);
+      cuda_check(cudaMemsetAsync(at(B.dk), 0, kvb, s), "memset dk");
+      cuda_check(cudaMemsetAsync(at(B.dv), 0, kvb, s), "memset dv");
+      ok(cad_ca_bwd(plan[h], at(B.q), at(B.k), at(B.v), at(B.o), at<float>(B.lse), at(B.dout), at(B.dq), at(B.dk),
+                    at(B.dv), ws[h], ws_bytes[h], s),
+         "cad_ca_bwd");
+      launches += 3;
+    }
+  }
+
+  void ret(int l, int h, int what, const cad_layer_io* io, cudaStream_t s, cudaStream_t local) {
+    const Bufs& B = b(l, h);
+    const i64 qr = std::max<i64>(1, mine.half[h].q_rows);
+    if (what == CAD_RETURN_O) {
+      if (flagged()) {
+        push(h, kXO, at(B.o), q_row, [&](int p) { return peer[static_cast<size_t>(p)].o; }, s, local);
+        push_lse(h, at<float>(B.lse), qr, s, local);
+        signal(F_O, h, gl(l), s);
+      } else if (move) {
+        nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s);
+        nccl_lse(h, at<float>(B.lse), qr, io->lse, mine.home_rows, s);
+      }
+    } else if (what == CAD_RETURN_GRAD) {
+      if (flagged()) {
+        push(h, kXO, at(B.dq), q_row, [&](int p) { return peer[static_cast<size_t>(p)].dq; }, s, local);
+        push(h, kXKR, at(B.dk), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdk); }, s, local);
+        push(h, kXKR, at(B.dv), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdv); }, s, local);
+        signal(F_G, h, gb(l), s);
+      } else if (move) {
+        nccl_rows(h, kXO, at(B.dq), q_row, io->dq, false, s);
+        nccl_rows(h, kXKR, at(B.dk), kv_row, at(B.sdk), true, s);  // partials land in recv order
+        nccl_rows(h, kXKR, at(B.dv), kv_row, at(B.sdv), true, s);
+      }
+    } else {
+      throw cad::DomainError("unknown return kind");
+    }
+  }
+
+  void finish(const cad_layer_io* io, cudaStream_t s) {
+    if (flagged())
+      for (int h = 0; h < 2; ++h) {
+        await(F_O, h, gl(NL - 1), s);
+        await(F_G, h, gb(0), s);
+      }
+    float* dk_acc = io->dk_acc ? io->dk_acc : acc_own[0];
+    float* dv_acc = io->dv_acc ? io->dv_acc : acc_own[1];
+    const i64 elems = mine.home_rows * hkv * d;
+    if (elems > 0) {
+      cuda_check(cudaMemsetAsync(dk_acc, 0, static_cast<size_t>(elems) * 4, s), "memset dk_acc");
+      cuda_check(cudaMemsetAsync(dv_acc, 0, static_cast<size_t>(elems) * 4, s), "memset dv_acc");
+    }
+    if (move)
+      for (int l = NL - 1; l >= 0; --l)
+        for (int h = 0; h < 2; ++h) {
+          const i64 n = mine.half[h].x[kXKR].n_recv();
+          if (!n) continue;
+          const Bufs& B = b(l, h);
+          ok(cad_scatter_add_bf16(at(B.sdk), d_recv_idx[h][kXKR], n, hkv * d, dk_acc, s), "scatter_add dk");
+          ok(cad_scatter_add_bf16(at(B.sdv), d_recv_idx[h][kXKR], n, hkv * d, dv_acc, s), "scatter_add dv");
+          launches += 2;
+        }
+    if (elems > 0 && io->dk) {
+      ok(cad_f32_to_bf16(dk_acc, elems, io->dk, s), "f32_to_bf16 dk");
+      ++launches;
+    }
+    if (elems > 0 && io->dv) {
+      ok(cad_f32_to_bf16(dv_acc, elems, io->dv, s), "f32_to_bf16 dv");
+      ++launches;
+    }
+    if (flagged()) signal(F_DONE, 0, gdone(), s);
+  }
+
+  // ------------------------------------------------------------- one step
+  // Event slots: [0] start, [1] comm done, then per (layer, half) 4 slots:
+  // QKV arrived, dO arrived, forward done, backward done.
+  int slot(int l, int h, int k) const { return 2 + ((l * 2 + h) * 4 + k); }
+
+  void step(const cad_layer_io* io, int mode, cudaStream_t comp) {
+    need_ready();
+    if (mode == CAD_STEP_COMPUTE) {
+      for (int l = 0; l < NL; ++l)
+        for (int h = 0; h < 2; ++h) compute(l, h, false, comp, false, true);
+      for (int l = NL - 1; l >= 0; --l)
+        for (int h = 0; h < 2; ++h) compute(l, h, true, comp, false, true);
+      return;
+    }
+    if (mode == CAD_STEP_SIGNAL && !flagged()) throw cad::ConfigError("signal mode needs the LOCAL or IPC transport");
+    if (mode < CAD_STEP_PINGPONG || mode > CAD_STEP_SIGNAL) throw cad::DomainError("unknown step mode");
+    check_io(io, true);
+    const bool run = mode != CAD_STEP_COMM;
+    move = mode != CAD_STEP_SIGNAL;
+    cudaStream_t comm = mode == CAD_STEP_SERIAL ? comp : comm_stream;
+    struct Restore {
+      cad_layer_ctx* c;
+      ~Restore() { c->move = true; }
+    } restore{this};
+    cuda_check(cudaEventRecord(event(0), comp), "event");
+    cuda_check(cudaStreamWaitEvent(comm, event(0), 0), "wait");
+    begin(comm);
+    auto disp = [&](int l, int h, int what) {
+      dispatch(l, h, what, io, comm, comp);
+      cuda_check(cudaEventRecord(event(slot(l, h, what == CAD_DISPATCH_QKV ? 0 : 1)), comm), "event");
+    };
+    auto ca = [&](int l, int h, bool bwd) {
+      cuda_check(cudaStreamWaitEvent(comp, event(slot(l, h, bwd ? 1 : 0)), 0), "wait");
+      compute(l, h, bwd, comp, true, run);
+      cuda_check(cudaEventRecord(event(slot(l, h, bwd ? 3 : 2)), comp), "event");
+    };
+    auto back = [&](int l, int h, int what) {
+      cuda_check(cudaStreamWaitEvent(comm, event(slot(l, h, what == CAD_RETURN_O ? 2 : 3)), 0), "wait");
+      ret(l, h, what, io, comm, comp);
+    };
+    // forward: comm D(0,0) D(1,0) dO(.,L-1) | R(0,l) D(0,l+1) | R(1,l) D(1,l+1) ...
+    //          comp       F(0,0)    F(1,0)      F(0,l+1)         F(1,l+1)
+    // so the return of half h and the next dispatch hide under CA(1-h)
+    // (the reference's windows, P/src/sim.cpp:69-72)
+    disp(0, 0, CAD_DISPATCH_QKV);
+    ca(0, 0, false);
+    disp(0, 1, CAD_DISPATCH_QKV);
+    disp(NL - 1, 0, CAD_DISPATCH_DO);  // the loss gradient of the top layer
+    disp(NL - 1, 1, CAD_DISPATCH_DO);
+    ca(0, 1, false);
+    for (int l = 0; l < NL; ++l)
+      for (int h = 0; h < 2; ++h) {
+        back(l, h, CAD_RETURN_O);
+        if (l + 1 < NL) {
+          disp(l + 1, h, CAD_DISPATCH_QKV);
+          ca(l + 1, h, false);
+        }
+      }
+    // backward, top layer first: G(h,l) then dO(h,l-1) under the other half's CA
+    ca(NL - 1, 0, true);
+    ca(NL - 1, 1, true);
+    for (int l = NL - 1; l >= 0; --l)
+      for (int h = 0; h < 2; ++h) {
+        back(l, h, CAD_RETURN_GRAD);
+        if (l > 0) {
+          disp(l - 1, h, CAD_DISPATCH_DO);
+          ca(l - 1, h, true);
+        }
+      }
+    cuda_check(cudaEventRecord(event(1), comm), "event");
+    cuda_check(cudaStreamWaitEvent(comp, event(1), 0), "wait");
+    finish(io, comp);
+  }
+
+  ~cad_layer_ctx() {  // runs with the context's device current
+    for (void* base : opened) cudaIpcCloseMemHandle(base);
+    for (int h = 0; h < 2; ++h) {
+      if (plan[h]) cad_ca_plan_destroy(plan[h]);
+      cudaFree(ws[h]);
+      for (int x = 0; x < 4; ++x) {
+        cudaFree(d_send_idx[h][x]);
+        cudaFree(d_recv_idx[h][x]);
+      }
+      cudaFree(acc_own[h]);
+    }
+    cudaFree(arena);
+    cudaFree(xsend);
+    cudaFree(xrecv);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+  }
+};
+
+extern "C" {
+
+int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64_t n_items, const cad_layer_cfg* cfg,
+                         cad_layer_ctx** out) {
+  return cad::guarded([&] {
+    if (!plan || !cfg || !out || (n_items > 0 && !home_items)) throw cad::DomainError("null argument");
+    *out = nullptr;
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) throw cad::DomainError("rank out of range");
+    if (cfg->head_dim != 128) throw cad::ConfigError("head_dim must be 128");
+    if (cfg->h_q < 1 || cfg->h_kv < 1 || cfg->h_q % cfg->h_kv) throw cad::ConfigError("h_q must be a multiple of h_kv");
+    if (cfg->transport < CAD_TRANSPORT_LOCAL || cfg->transport > CAD_TRANSPORT_NCCL)
+      throw cad::ConfigError("unknown transport");
+    if (cfg->layers < 1) throw cad::ConfigError("layers must be >= 1");
+    cad_plan_stats st;
+    ok(cad_plan_get_stats(plan, &st), "cad_plan_get_stats");
+    if (st.n_servers != cfg->world) throw cad::ConfigError("plan servers != world");
+    auto C = std::make_unique<cad_layer_ctx>();
+    C->cfg = *cfg;
+    cuda_check(cudaGetDevice(&C->device), "cudaGetDevice");
+    C->W = cfg->world;
+    C->me = cfg->rank;
+    C->NL = cfg->layers;
+    C->hq = cfg->h_q;
+    C->hkv = cfg->h_kv;
+    C->q_row = C->hq * C->d * 2;
+    C->kv_row = C->hkv * C->d * 2;
+    C->lse_row = C->hq * 4;
+    // every rank's rows: ours in full, the peers' for where our rows land
+    std::vector<RankRows> all;
+    for (int r = 0; r < C->W; ++r)
+      all.push_back(read_rank(plan, home_items, n_items, r, C->q_row, C->kv_row, cfg->balance_halves));
+    C->mine = all[static_cast<size_t>(C->me)];
+    C->layout = layout_of(C->mine, C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
+    C->peer.resize(static_cast<size_t>(C->W));
+    for (int p = 0; p < C->W; ++p) {
+      Peer& P = C->peer[static_cast<size_t>(p)];
+      P.home_rows = all[static_cast<size_t>(p)].home_rows;
+      P.layout = layout_of(all[static_cast<size_t>(p)], C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
+    }
+    // push runs: my send rows to p against p's receive rows from me
+    for (int h = 0; h < 2; ++h)
+      for (int x = 0; x < 4; ++x) {
+        const XferRows& M = C->mine.half[h].x[x];
+        auto& R = C->runs[h][x];
+        auto& off = C->run_off[h][x];
+        off.assign(1, 0);
+        i64 so = 0;
+        for (int p = 0; p < C->W; ++p) {
+          const XferRows& PX = all[static_cast<size_t>(p)].half[h].x[x];
+          i64 ro = 0;
+          for (int q = 0; q < C->me; ++q) ro += PX.recv_counts[static_cast<size_t>(q)];
+          const i64 n = M.send_counts[static_cast<size_t>(p)];
+          if (PX.recv_counts[static_cast<size_t>(C->me)] != n) throw cad::DomainError("row plans disagree");
+          std::vector<i64> dst(static_cast<size_t>(n));
+          for (i64 i = 0; i < n; ++i)
+            dst[static_cast<size_t>(i)] = x == kXKR ? ro + i : PX.recv_idx[static_cast<size_t>(ro + i)];
+          const auto rr = make_runs(M.send_idx.data() + so, dst.data(), n);
+          R.insert(R.end(), rr.begin(), rr.end());
+          off.push_back(R.size());
+          so += n;
+        }
+      }
+    all.clear();
+    // server CA plans and workspaces
+    size_t xmax = 16;
+    for (int h = 0; h < 2; ++h) {
+      const HalfRows& H = C->mine.half[h];
+      for (const cad_ca_task& t : H.tasks) C->pairs += cad_causal_pairs(t.n_q, t.kv_len);
+      for (int x = 0; x < 4; ++x) {
+        C->d_send_idx[h][x] = dev_copy(H.x[x].send_idx);
+        C->d_recv_idx[h][x] = dev_copy(H.x[x].recv_idx);
+        xmax = std::max(xmax, static_cast<size_t>(std::max(H.x[x].n_send(), H.x[x].n_recv()) * C->q_row));
+      }
+      if (H.tasks.empty()) continue;
+      cad_ca_shape sh{};
+      sh.h_q = cfg->h_q;
+      sh.h_kv = cfg->h_kv;
+      sh.head_dim = 128;
+      sh.softmax_scale = cfg->softmax_scale;
+      sh.q_rows = std::max<i64>(1, H.q_rows);
+      sh.kv_rows = std::max<i64>(1, H.kv_rows);
+      ok(cad_ca_plan_create(H.tasks.data(), static_cast<i64>(H.tasks.size()), &sh, &C->plan[h]), "cad_ca_plan_create");
+      if (cfg->reserve_sms > 0) {
+        int sms = 148;
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C->device), "sm count");
+        ok(cad_ca_plan_set_max_ctas(C->plan[h], std::max(2, sms - cfg->reserve_sms)), "set_max_ctas");
+      }
+      cad_ca_plan_info info;
+      ok(cad_ca_plan_info_get(C->plan[h], &info), "cad_ca_plan_info_get");
+      C->ws_bytes[h] = std::max<size_t>(16, info.workspace_bytes);
+      cuda_check(cudaMalloc(&C->ws[h], C->ws_bytes[h]), "cudaMalloc(workspace)");
+    }
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&C->arena), C->layout.total), "cudaMalloc(server buffers)");
+    C->flags = C->at<int32_t>(C->layout.flags);
+    cuda_check(cudaMemset(C->flags, 0, static_cast<size_t>(4) * 2 * kKinds * C->W), "memset flags");
+    const size_t acc = static_cast<size_t>(std::max<i64>(1, C->mine.home_rows * C->hkv * C->d)) * 4;
+    for (int i = 0; i < 2; ++i) cuda_check(cudaMalloc(reinterpret_cast<void**>(&C->acc_own[i]), acc), "cudaMalloc(acc)");
+    if (cfg->transport == CAD_TRANSPORT_NCCL) {
+      C->xbytes = xmax;
+      cuda_check(cudaMalloc(&C->xsend, xmax), "cudaMalloc(send)");
+      cuda_check(cudaMalloc(&C->xrecv, xmax), "cudaMalloc(recv)");
+    }
+    cuda_check(cudaStreamCreateWithFlags(&C->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    C->ev.resize(static_cast<size_t>(2 + 8 * C->NL));
+    for (cudaEvent_t& e : C->ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    *out = C.release();
+  });
+}
+
+int cad_layer_ctx_info_get(const cad_layer_ctx* ctx, cad_layer_ctx_info* info) {
+  return cad::guarded([&] {
+    if (!ctx || !info) throw cad::DomainError("null argument");
+    *info = cad_layer_ctx_info{};
+    info->home_rows = ctx->mine.home_rows;
+    for (int h = 0; h < 2; ++h) {
+      info->q_rows[h] = ctx->mine.half[h].q_rows;
+      info->kv_rows[h] = ctx->mine.half[h].kv_rows;
+      info->n_tasks[h] = static_cast<int64_t>(ctx->mine.half[h].tasks.size());
+      for (int x = 0; x < 4; ++x) info->wire_bytes[h][x] = ctx->mine.half[h].wire[x];
+    }
+    info->served_pairs = ctx->pairs;
+    info->blob_bytes = sizeof(Blob);
+    info->launches = ctx->launches;
+  });
+}
+
+int cad_layer_ctx_bind_outputs(cad_layer_ctx* ctx, void* o, float* lse, void* dq) {
+  return cad::guarded([&] {
+    if (!ctx || !o || !lse || !dq) throw cad::DomainError("null argument");
+    if (ctx->connected) throw cad::ConfigError("outputs must be bound before export/connect");
+    ctx->o_home = o;
+    ctx->lse_home = lse;
+    ctx->dq_home = dq;
+  });
+}
+
+int cad_layer_ctx_export(cad_layer_ctx* ctx, void* blob, size_t cap, size_t* need) {
+  return cad::guarded([&] {
+    if (!ctx || !need) throw cad::DomainError("null argument");
+    *need = sizeof(Blob);
+    if (!blob || cap < sizeof(Blob)) throw cad::CapacityError("blob buffer too small");
+    if (ctx->cfg.transport == CAD_TRANSPORT_NCCL) throw cad::ConfigError("NCCL transport has nothing to export");
+    if (!ctx->o_home) throw cad::ConfigError("bind the home outputs before export");
+    cad_dev::DeviceGuard dg(ctx->device);
+    Blob B{};
+    B.magic = kBlobMagic;
+    B.rank = ctx->me;
+    B.world = ctx->W;
+    B.transport = ctx->cfg.transport;
+    B.layers = ctx->NL;
+    B.home_rows = ctx->mine.home_rows;
+    const void* ptrs[4] = {ctx->arena, ctx->o_home, ctx->lse_home, ctx->dq_home};
+    for (int i = 0; i < 4; ++i) {
+      B.ref[i].raw = reinterpret_cast<uint64_t>(ptrs[i]);
+      if (ctx->cfg.transport == CAD_TRANSPORT_IPC) ok(cad_ipc_handle(ptrs[i], B.ref[i].handle, &B.ref[i].offset), "ipc");
+    }
+    std::memcpy(blob, &B, sizeof(B));
+  });
+}
+
+int cad_layer_ctx_connect(cad_layer_ctx* ctx, const void* blobs, size_t blob_bytes) {
+  return cad::guarded([&] {
+    if (!ctx || !blobs) throw cad::DomainError("null argument");
+    if (ctx->cfg.transport == CAD_TRANSPORT_NCCL) throw cad::ConfigError("NCCL transport: use cad_layer_ctx_set_comm");
+    if (blob_bytes != sizeof(Blob)) throw cad::DomainError("blob size mismatch");
+    if (ctx->connected) throw cad::ConfigError("already connected");
+    cad_dev::DeviceGuard dg(ctx->device);
+    std::map<std::string, char*> mapped;
+    for (int p = 0; p < ctx->W; ++p) {
+      Blob B;
+      std::memcpy(&B, static_cast<const char*>(blobs) + static_cast<size_t>(p) * sizeof(Blob), sizeof(Blob));
+      if (B.magic != kBlobMagic || B.rank != p || B.world != ctx->W || B.layers != ctx->NL ||
+          B.transport != ctx->cfg.transport)
+        throw cad::DomainError("blob of rank " + std::to_string(p) + " does not match this context");
+      Peer& P = ctx->peer[static_cast<size_t>(p)];
+      if (B.home_rows != P.home_rows) throw cad::DomainError("peer home rows disagree with the row plan");
+      char* ptr[4];
+      for (int i = 0; i < 4; ++i) {
+        if (p == ctx->me || ctx->cfg.transport == CAD_TRANSPORT_LOCAL) {
+          ptr[i] = reinterpret_cast<char*>(B.ref[i].raw);
+          continue;
+        }
+        const std::string key(reinterpret_cast<const char*>(B.ref[i].handle), 64);
+        auto it = mapped.find(key);
+        if (it == mapped.end()) {
+          void* base = nullptr;
+          ok(cad_ipc_open(B.ref[i].handle, &base), "cad_ipc_open");
+          ctx->opened.push_back(base);
+          it = mapped.emplace(key, static_cast<char*>(base)).first;
+        }
+        ptr[i] = it->second + B.ref[i].offset;
+      }
+      P.arena = ptr[0];
+      P.o = ptr[1];
+      P.lse = reinterpret_cast<float*>(ptr[2]);
+      P.dq = ptr[3];
+    }
+    ctx->connected = true;
+  });
+}
+
+int cad_layer_ctx_set_comm(cad_layer_ctx* ctx, cad_comm* comm) {
+  return cad::guarded([&] {
+    if (!ctx || !comm) throw cad::DomainError("null argument");
+    if (ctx->cfg.transport != CAD_TRANSPORT_NCCL) throw cad::ConfigError("not an NCCL-transport context");
+    ctx->comm = comm;
+  });
+}
+
+int cad_layer_ctx_destroy(cad_layer_ctx* ctx) {
+  return cad::guarded([&] {
+    if (!ctx) return;
+    cad_dev::DeviceGuard dg(ctx->device);
+    delete ctx;
+  });
+}
+
+int cad_layer_begin(cad_layer_ctx* ctx, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    cad_dev::DeviceGuard dg(ctx->device);
+    ctx->begin(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cad_dispatch(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what, const cad_layer_io* io, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->check_lh(layer, half);
+    ctx->check_io(io, false);
+    ctx->need_ready();
+    cad_dev::DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->dispatch(layer, half, what, io, s, s);
+  });
+}
+
+int cad_dispatch_ex(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what, const cad_layer_io* io,
+                    void* stream, void* local_stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->check_lh(layer, half);
+    ctx->check_io(io, false);
+    ctx->need_ready();
+    cad_dev::DeviceGuard dg(ctx->device);
+    ctx->dispatch(layer, half, what, io, static_cast<cudaStream_t>(stream), static_cast<cudaStream_t>(local_stream));
+  });
+}
+
+int cad_layer_compute(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t backward, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->check_lh(layer, half);
+    ctx->need_ready();
+    cad_dev::DeviceGuard dg(ctx->device);
+    ctx->compute(layer, half, backward != 0, static_cast<cudaStream_t>(stream), true, true);
+  });
+}
+
+int cad_return(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what, const cad_layer_io* io, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->check_lh(layer, half);
+    ctx->check_io(io, true);
+    ctx->need_ready();
+    cad_dev::DeviceGuard dg(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->ret(layer, half, what, io, s, s);
+  });
+}
+
+int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->check_io(io, false);
+    ctx->need_ready();
+    cad_dev::DeviceGuard dg(ctx->device);
+    ctx->finish(io, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode, void* stream) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    cad_dev::DeviceGuard dg(ctx->device);
+    ctx->step(io, mode, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"
