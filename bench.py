@@ -90,23 +90,32 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU legs
-def cpu_sample_tasks():
-    """Bounded CPU sample of the config-2 workload: one KV-head group (4 query
-    heads of one KV head) of the batch's first documents, cut to 6144 tokens."""
-    from paper_2510_18121_b200 import configs as CF
-    from paper_2510_18121_b200 import scheduler as S
-    lengths = S.sample_batch(CF.length_dist("pretrain", SEED), 131072)
-    cut, out = 6144, []
-    for l in lengths:
-        take = min(l, cut - sum(out))
-        if take <= 0:
-            break
-        out.append(take)
-    return out
+# Both CPU legs (cpu_baseline and --impl reference) time the SAME sample:
+# BASELINE config 1 (docs 4096 + 4 x 1024 in one 8192-token
+# chunk, d=128, fp32 fwd+bwd) one attention head at a time -- its 8 heads are
+# independent (8 Q / 8 KV heads) -- through the CPU oracle port
+# (oracle/ca_oracle.c; the reference is an analytical simulator with no CA
+# numerics). cpu_baseline runs all 8 heads (= config 1 in full); the
+# reference arm runs one head per step. Neither leg loads libcad.so: lengths
+# are fixed and the scheduler timing uses the reference's own sampler,
+# placement and schedule() (oracle/_ref/libcadsim_ref.so).
+CFG1_LENGTHS = [4096, 1024, 1024, 1024, 1024]  # P/tests/test_scheduler.cpp:133-135
+CFG1_HEADS = 8
 
 
-def run_cpu_oracle(lengths, h_q=4, h_kv=1, threads=0, reps=1):
-    """Times the oracle fwd+bwd; returns (TFLOP/s, seconds, threads)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_cpu_oracle(lengths, h_q=1, h_kv=1, threads=0, reps=1):
+    """Times the oracle fwd+bwd; returns (TFLOP/s, seconds per rep, threads)."""
     import numpy as np
     import oracle
     T = sum(lengths)
@@ -130,30 +139,78 @@ def run_cpu_oracle(lengths, h_q=4, h_kv=1, threads=0, reps=1):
     return flops / dt / 1e12, dt, nthreads
 
 
+def ref_scheduler_ms_cfg3():
+    """The reference's schedule() wall time on the 8-GPU config-3 plan
+    (512K tokens, pretrain_upsampled seed 1, 8B sizes), the reference's own
+    sample_batch/place_sequential producing the items."""
+    import ctypes as C
+    import math
+    import oracle
+    from paper_2510_18121_b200 import _native as N  # struct layouts only; libcad.so is not loaded
+    R = oracle.ref_lib()
+    d = N.cad_length_dist()
+    d.kind, d.max_doc_len, d.min_len_threshold, d.seed = 0, 131072, 32768, SEED
+    d.log_mu, d.log_sigma, d.upsample_drop_prob = math.log(2048.0), 1.4, 0.9
+    d.long_mix_weight, d.long_log_mu, d.long_log_sigma = 0.3, math.log(65536.0), 0.7
+    d.fixed_len, d.uniform_min = 1024, 1
+    total, G = 524288, 8
+    n = N.i64()
+    assert R.ref_sample_batch(C.byref(d), total, None, 0, C.byref(n)) == 0
+    lens = (N.i64 * n.value)()
+    assert R.ref_sample_batch(C.byref(d), total, lens, n.value, C.byref(n)) == 0
+    m = N.i64()
+    assert R.ref_place_sequential(lens, n.value, G, total // G, None, 0, C.byref(m)) == 0
+    items = (N.cad_item * m.value)()
+    assert R.ref_place_sequential(lens, n.value, G, total // G, items, m.value, C.byref(m)) == 0
+    cfg = N.cad_sched_cfg()
+    cfg.epsilon, cfg.e_threshold, cfg.tile_size, cfg.alpha_ca = 0.0, 0.01, 128, 1.0
+    cfg.size_q, cfg.size_kv, cfg.double_query_head_tail, cfg.max_moves = 8192, 4096, 0, 1 << 20
+    reps = 200
+    secs = R.ref_schedule_seconds(items, m.value, G, C.byref(cfg), reps)
+    return {"ms": secs / reps * 1e3, "items": m.value, "docs": n.value, "servers": G,
+            "what": "reference schedule() (libcadsim_ref.so) on config 3: 512K tokens, 8 servers, "
+                    "pretrain_upsampled seed 1, single thread"}
+
+
+def _cfg1_sample(heads):
+    return (f"BASELINE config 1 (docs {CFG1_LENGTHS}, 8192 tokens, d=128, fp32 IO / fp64 accumulate) "
+            f"fwd+bwd through the oracle port oracle/ca_oracle.c, {heads} of its {CFG1_HEADS} independent "
+            "heads")
+
+
 def reference_arm(args, rank):
-    """--impl reference: the reference's CPU path on the host cores."""
+    """--impl reference: the reference's CPU path on the host cores (rank 0
+    only). Each step = config 1, one head (the same sample cpu_baseline times
+    all 8 heads of). Loads only oracle/_ref/*."""
     if rank != 0:
         return
-    lengths = cpu_sample_tasks()[:1]
-    lengths = [min(lengths[0], 2048)]
     vals, nth = [], 0
     for i in range(args.warmup + args.steps):
-        tf, dt, nth = run_cpu_oracle(lengths)
+        tf, dt, nth = run_cpu_oracle(CFG1_LENGTHS)
         if i >= args.warmup:
             vals.append((tf, dt))
     tf = statistics.mean(v[0] for v in vals)
     ms = statistics.mean(v[1] for v in vals) * 1e3
-    sample = (f"oracle port (oracle/ca_oracle.c, fp32 IO/fp64 accumulate) fwd+bwd of one {lengths[0]}-token "
-              f"document, 4 query heads / 1 KV head, d=128, per step")
+    sample = _cfg1_sample(1) + " per step"
+    try:
+        sched = ref_scheduler_ms_cfg3()
+    except Exception as e:  # reference library absent
+        sched = f"unavailable: {e}"
+    cfg2_flops = 297.9e12  # config 2 seed 1, 14 d H_q P (SURVEY.md 8d)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": "config 2 sample (CPU-bounded)", "sample": sample},
-        "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": nth,
-                         "kind": "port", "sample": sample},
+        "config": {"workload": CFG2_WORKLOAD, "sample": sample,
+                   "extrapolated_config2_step_s": cfg2_flops / (tf * 1e12) if tf > 0 else None},
+        "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": nth, "cpu_model": cpu_model(),
+                         "kind": "port", "sample": sample, "scheduler_ref": sched},
         "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+CFG2_WORKLOAD = ("BASELINE config 2: Llama-3-8B CA (32 Q / 8 KV heads, d=128), 131072 packed tokens, "
+                 "pretrain_upsampled docs seed 1, one layer fwd+bwd")
 
 
 # --------------------------------------------------------------------------- GPU, N=1
@@ -225,12 +282,13 @@ def single_gpu(args):
 
     # end to end through the public API: pinned host inputs in, grads out
     hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
-    hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (dq, dk, dv))
+    # every output comes back: O and LSE (forward) and dQ, dK, dV (backward)
+    host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (o, lse, dq, dk, dv)]
     h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, hdo))
-    d2h = sum(t.numel() * t.element_size() for t in (hdq, hdk, hdv))
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
 
     # Double-buffered: step j's inputs go host -> device on a copy stream while
-    # step j-1 computes, and step j's gradients come back while step j+1
+    # step j-1 computes, and step j's outputs come back while step j+1
     # computes; every step still moves its own inputs and results.
     sets = [(q, k, v, do, o, lse, dq, dk, dv),
             tuple(torch.empty_like(t) for t in (q, k, v, do, o, lse, dq, dk, dv))]
@@ -256,7 +314,7 @@ def single_gpu(args):
                 with torch.cuda.stream(copy):
                     copy.wait_event(comp_done[(j - 1) % 2])
                     b = sets[(j - 1) % 2]
-                    for dst, src in zip((hdq, hdk, hdv), b[6:]):
+                    for dst, src in zip(host_out, b[4:]):
                         dst.copy_(src, non_blocking=True)
             if j < n:  # compute step j
                 b = sets[j % 2]
@@ -291,23 +349,20 @@ def single_gpu(args):
 
     cpu = None
     if not args.no_cpu:
-        sample = cpu_sample_tasks()
-        tf, dt, nth = run_cpu_oracle(sample)
-        cpu = {"value": tf, "unit": "TFLOP/s", "cores": nth, "kind": "port",
-               "sample": f"oracle fwd+bwd of docs {sample} (first 6144 tokens of the batch), "
-                         f"4 query heads of 1 KV head, {dt:.1f} s"}
-        # reference scheduler on the same batch (the reference's own CPU code)
+        tf, dt, nth = run_cpu_oracle(CFG1_LENGTHS, reps=CFG1_HEADS)
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": nth, "cpu_model": cpu_model(), "kind": "port",
+               "sample": _cfg1_sample(CFG1_HEADS) + f" = config 1 in full, {dt * CFG1_HEADS:.1f} s",
+               "extrapolated_config2_step_s": flops["total"] / (tf * 1e12) if tf > 0 else None}
         try:
-            cpu["scheduler_ms_ref"] = ref_scheduler_ms(lengths, 1, shape)
+            cpu["scheduler_ref"] = ref_scheduler_ms_cfg3()
         except Exception as e:  # reference library absent
-            cpu["scheduler_ms_ref"] = f"unavailable: {e}"
+            cpu["scheduler_ref"] = f"unavailable: {e}"
 
     out = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "BASELINE config 2: Llama-3-8B CA (32 Q / 8 KV heads, d=128), 131072 packed "
-                               "tokens, pretrain_upsampled docs seed 1, one layer fwd+bwd",
+        "config": {"workload": CFG2_WORKLOAD,
                    "docs": lengths, "causal_pairs": plan.causal_pairs, "flops_per_step": flops["total"],
                    "l2": "inputs larger than L2 (Q alone is 1 GiB)", "parallelism": "single GPU"},
         "per_gpu_tflops": value, "pct_bf16_peak": value / peak, "pct_bf16_peak_sustained": value / peak_sus,
@@ -321,20 +376,6 @@ def single_gpu(args):
         "clocks": clk,
     }
     print(json.dumps(out))
-
-
-def ref_scheduler_ms(lengths, n_gpus, shape):
-    import ctypes as C
-    import oracle
-    from paper_2510_18121_b200 import configs as CF
-    from paper_2510_18121_b200 import scheduler as S
-    from paper_2510_18121_b200 import _native as N
-    T = sum(lengths)
-    items = S.place_sequential(lengths, n_gpus, T // n_gpus)
-    arr = (N.cad_item * len(items))(*[i.to_c() for i in items])
-    reps = 200
-    secs = oracle.ref_lib().ref_schedule_seconds(arr, len(items), n_gpus, C.byref(CF.sched_config(shape).to_c()), reps)
-    return secs / reps * 1e3
 
 
 def main():

@@ -468,7 +468,9 @@ int cad_alltoallv(cad_comm* comm, const void* send, const int64_t* send_bytes,
 #define CAD_TRANSPORT_LOCAL 0 /* every rank's context lives in this process
                                  (one GPU, or GPUs with peer access): peers'
                                  buffers are addressed directly; the same
-                                 copy/flag code path as IPC */
+                                 copy/flag code path as IPC. Driven phase by
+                                 phase in dependency order across the ranks
+                                 (cad_layer_step refuses: CAD_ERR_CONFIG) */
 #define CAD_TRANSPORT_IPC 1   /* one process per GPU: each rank pushes its
                                  rows into the peers' buffers (CUDA IPC
                                  mappings, copy engines) and signals arrival
@@ -575,7 +577,8 @@ int cad_return(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
 int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
 
 /* One whole step (all layers, forward + backward) on `stream` (compute) and
- * the context's comm stream, in the reference's ping-pong windows. */
+ * the context's comm stream, in the reference's ping-pong windows. IPC and
+ * NCCL transports (one process per rank); LOCAL only in COMPUTE mode. */
 #define CAD_STEP_PINGPONG 0 /* comm of one half under CA of the other */
 #define CAD_STEP_SERIAL 1   /* everything on `stream`, no overlap */
 #define CAD_STEP_COMPUTE 2  /* CA kernels only (server buffers as resident) */

@@ -786,6 +786,15 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
 
 }  // namespace dq
 }  // namespace bwd
+
+void preload_bwd() {
+  set_max_smem(reinterpret_cast<const void*>(bwd::kv::ca_bwd_dkdv_kernel), bwd::kv::kSmemBytes,
+               "cudaFuncSetAttribute(dkdv)");
+  set_max_smem(reinterpret_cast<const void*>(bwd::dq::ca_bwd_dq_kernel), bwd::dq::kSmemBytes,
+               "cudaFuncSetAttribute(dq)");
+  cudaFuncAttributes a;
+  cuda_check(cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(bwd::ca_delta_kernel)), "load delta");
+}
 }  // namespace cad_dev
 
 extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const void* k,

@@ -109,6 +109,18 @@ void cuda_check(cudaError_t e, const char* what);
 // the attribute belongs to the current device's context, so a process that
 // drives several GPUs through the C-ABI needs it on each of them. Thread-safe.
 void set_max_smem(const void* kernel, int bytes, const char* what);
+// Loads every kernel of the library on the current device (once per device):
+// with CUDA's lazy module loading the first launch of a kernel loads its
+// module, which can block the host until the device is idle -- a deadlock
+// when the device waits on work this host thread has yet to enqueue (several
+// ranks' contexts driven from one thread). Called at plan/context creation.
+void preload_kernels();
+void preload_fwd();
+void preload_fwd2();
+void preload_bwd();
+void preload_dkdv2();
+void preload_dq2();
+void preload_comm();
 // Makes the plan's device current for the duration of a launch (and restores
 // the caller's device), so one host thread may drive plans on several GPUs.
 struct DeviceGuard {

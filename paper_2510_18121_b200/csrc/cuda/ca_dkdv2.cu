@@ -509,6 +509,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdv_pair_kernel(const __g
 
 }  // namespace kv2
 
+void preload_dkdv2() {
+  set_max_smem(reinterpret_cast<const void*>(kv2::ca_bwd_dkdv_pair_kernel), kv2::kSmemBytes,
+               "cudaFuncSetAttribute(dkdv2)");
+}
+
 // Launch of the pair dK/dV kernel (cluster dims 2); false if the plan has no pair units.
 bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
                       const float* nlse2, const float* ndelta, int64_t pitch, void* dk, void* dv,

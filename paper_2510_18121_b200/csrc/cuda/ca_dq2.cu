@@ -353,6 +353,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
 
 }  // namespace dq2
 
+void preload_dq2() {
+  set_max_smem(reinterpret_cast<const void*>(dq2::ca_bwd_dq_pair_kernel), dq2::kSmemBytes,
+               "cudaFuncSetAttribute(dq2)");
+}
+
 // Launch of the pair dQ kernel (cluster dims 2); false if the plan has no pair units.
 bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
                     const float* lse2, const float* delta, int64_t pitch, void* dq, cudaStream_t stream) {

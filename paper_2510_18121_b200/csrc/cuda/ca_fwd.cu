@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_kernel(const __grid_consta
 
 }  // namespace fwd
 
+void preload_fwd() {
+  set_max_smem(reinterpret_cast<const void*>(fwd::ca_fwd_kernel), fwd::kSmemBytes, "cudaFuncSetAttribute(fwd)");
+}
+
 }  // namespace cad_dev
 
 extern "C" int cad_ca_fwd(const cad_ca_plan* plan, const void* q, const void* k, const void* v,

@@ -326,6 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_fwd_pair_kernel(const __grid_c
 
 }  // namespace fwd2
 
+void preload_fwd2() {
+  set_max_smem(reinterpret_cast<const void*>(fwd2::ca_fwd_pair_kernel), fwd2::kSmemBytes,
+               "cudaFuncSetAttribute(fwd2)");
+}
+
 // Launch of the pair kernel (cluster dims 2); false if this plan has no pair units.
 bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, void* o, float* lse,
                      cudaStream_t stream) {

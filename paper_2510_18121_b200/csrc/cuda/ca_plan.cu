@@ -53,6 +53,31 @@ void set_max_smem(const void* kernel, int bytes, const char* what) {
   done.insert(key);
 }
 
+void preload_kernels() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(dev)) return;
+  preload_fwd();
+  preload_fwd2();
+  preload_bwd();
+  preload_dkdv2();
+  preload_dq2();
+  preload_comm();
+  // the runtime's own memset / device-to-device copy kernels (the executor's
+  // cudaMemsetAsync, cudaMemcpyAsync and cudaMemcpy2DAsync)
+  char* p = nullptr;
+  cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), 4096), "cudaMalloc");
+  cuda_check(cudaMemsetAsync(p, 0, 4096, nullptr), "memset");
+  cuda_check(cudaMemcpyAsync(p + 2048, p, 1024, cudaMemcpyDeviceToDevice, nullptr), "memcpy");
+  cuda_check(cudaMemcpy2DAsync(p + 2048, 64, p, 128, 4, 8, cudaMemcpyDeviceToDevice, nullptr), "memcpy2d");
+  cuda_check(cudaStreamSynchronize(nullptr), "sync");
+  cudaFree(p);
+  done.insert(dev);
+}
+
 DeviceGuard::DeviceGuard(int device) : want(device) {
   cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
   if (prev != want) cuda_check(cudaSetDevice(want), "cudaSetDevice");
@@ -304,6 +329,7 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     }
     cad_dev::build_units(*P);
     cuda_check(cudaGetDevice(&P->device), "cudaGetDevice");
+    cad_dev::preload_kernels();
     cuda_check(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device),
                "cudaDeviceGetAttribute");
     auto upload = [](auto& vec, auto** dst) {

@@ -312,6 +312,16 @@ __global__ void __launch_bounds__(256) copy_spans_bulk_kernel(const cad_span* sp
   if (nb) flush();
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
 }
+void preload_comm() {
+  cudaFuncAttributes a;
+  for (const void* f : {reinterpret_cast<const void*>(gather_rows_kernel), reinterpret_cast<const void*>(scatter_rows_kernel),
+                        reinterpret_cast<const void*>(scatter_add_bf16_kernel),
+                        reinterpret_cast<const void*>(gather_cols_kernel),
+                        reinterpret_cast<const void*>(scatter_cols_kernel),
+                        reinterpret_cast<const void*>(f32_to_bf16_kernel), reinterpret_cast<const void*>(copy_spans_kernel)})
+    cuda_check(cudaFuncGetAttributes(&a, f), "load comm kernels");
+  set_max_smem(reinterpret_cast<const void*>(copy_spans_bulk_kernel), kBulkSmem, "cudaFuncSetAttribute(copy_spans_bulk)");
+}
 }  // namespace cad_dev
 
 extern "C" {

@@ -36,6 +36,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -54,7 +56,15 @@ constexpr int kXQ = CAD_XFER_Q, kXKV = CAD_XFER_KV, kXO = CAD_XFER_O_RET, kXKR =
 enum FlagKind { F_QKV = 0, F_DO = 1, F_O = 2, F_G = 3, F_DONE = 4, kKinds = 5 };
 constexpr uint32_t kBlobMagic = 0xCAD1A7E5u;
 
+// CAD_TRACE_HOST=1: every transport/compute call of a context logged on
+// stderr before it is issued (host-side debugging of enqueue order)
+bool trace_host() {
+  static const bool on = std::getenv("CAD_TRACE_HOST") != nullptr;
+  return on;
+}
+
 void ok(int rc, const char* what) {
+  if (trace_host()) std::fprintf(stderr, "[cad] issued %s rc=%d\n", what, rc);
   if (rc == CAD_OK) return;
   const std::string msg = std::string(what) + ": " + cad_last_error();
   switch (rc) {
@@ -252,9 +262,11 @@ struct cad_layer_ctx {
     return base + (kind * 2 + h) * W + src;
   }
   void signal(int kind, int h, uint32_t value, cudaStream_t s) const {
+    if (trace_host()) std::fprintf(stderr, "[cad] rank %d signal kind %d half %d value %u\n", me, kind, h, value);
     for (int p = 0; p < W; ++p) ok(cad_stream_write_u32(flag_of(p, kind, h, me), value, s), "signal");
   }
   void await(int kind, int h, uint32_t value, cudaStream_t s) const {
+    if (trace_host()) std::fprintf(stderr, "[cad] rank %d await kind %d half %d value %u\n", me, kind, h, value);
     for (int src = 0; src < W; ++src) ok(cad_stream_wait_u32(flag_of(me, kind, h, src), value, s), "await");
   }
   cudaEvent_t event(int slot) const { return ev[static_cast<size_t>(slot)]; }
@@ -465,6 +477,15 @@ struct cad_layer_ctx {
 
   void step(const cad_layer_io* io, int mode, cudaStream_t comp) {
     need_ready();
+    // One thread enqueueing a whole step of rank 0 before rank 1's puts GPU
+    // waits ahead of the work that releases them; streams of one context can
+    // share a hardware queue (CUDA_DEVICE_MAX_CONNECTIONS), so such a wait can
+    // hold up the very stream it waits for. LOCAL contexts are therefore
+    // driven phase by phase (cad_layer_begin / cad_dispatch / ... in
+    // dependency order across ranks), never by cad_layer_step.
+    if (cfg.transport == CAD_TRANSPORT_LOCAL && mode != CAD_STEP_COMPUTE)
+      throw cad::ConfigError("cad_layer_step needs one process per rank (IPC or NCCL transport); drive LOCAL "
+                             "contexts with the per-layer entry points in dependency order");
     if (mode == CAD_STEP_COMPUTE) {
       for (int l = 0; l < NL; ++l)
         for (int h = 0; h < 2; ++h) compute(l, h, false, comp, false, true);
@@ -570,6 +591,7 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     auto C = std::make_unique<cad_layer_ctx>();
     C->cfg = *cfg;
     cuda_check(cudaGetDevice(&C->device), "cudaGetDevice");
+    cad_dev::preload_kernels();
     C->W = cfg->world;
     C->me = cfg->rank;
     C->NL = cfg->layers;

@@ -16,11 +16,10 @@ def bf16_round(x):
     return torch.from_numpy(x).to(torch.bfloat16).float().numpy()
 
 
-def run_local(lengths, world, shape, seed=0, items=None, mode="phases", cfg=None, tokens_per_device=None):
-    """mode 'phases': the per-layer entry points (cad_layer_begin, cad_dispatch,
+def run_local(lengths, world, shape, seed=0, items=None, cfg=None, tokens_per_device=None):
+    """The per-layer entry points (cad_layer_begin, cad_dispatch,
     cad_layer_compute, cad_return, cad_layer_finish) called rank by rank in
-    dependency order on one stream; 'step': cad_layer_step per rank, each
-    rank on its own compute stream (ping-pong with the context's comm stream)."""
+    dependency order on one stream."""
     from paper_2510_18121_b200 import dispatch as D
     dev = torch.device("cuda", 0)
     plans = [D.LayerPlan(lengths, world, r, shape, cfg=cfg, items=items, tokens_per_device=tokens_per_device)
@@ -47,26 +46,21 @@ def run_local(lengths, world, shape, seed=0, items=None, mode="phases", cfg=None
     blobs = [L.export() for L in layers]
     for L in layers:
         L.connect(blobs)
-    if mode == "phases":
-        s = torch.cuda.current_stream(dev)
-        for L in layers:
-            L.begin(s)
-        for what, bwd, ret in ((D.DISPATCH_QKV, False, D.RETURN_O), (D.DISPATCH_DO, True, D.RETURN_GRAD)):
-            for h in (0, 1):
-                for r, L in enumerate(layers):
-                    L.dispatch(0, h, what, ios[r], s)
-            for h in (0, 1):
-                for L in layers:
-                    L.compute(0, h, bwd, s)
-            for h in (0, 1):
-                for r, L in enumerate(layers):
-                    L.ret(0, h, ret, ios[r], s)
-        for r, L in enumerate(layers):
-            L.finish(ios[r], s)
-    else:
-        streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
-        for r, L in enumerate(layers):
-            L.step(ios[r], "pingpong", streams[r])
+    s = torch.cuda.current_stream(dev)
+    for L in layers:
+        L.begin(s)
+    for what, bwd, ret in ((D.DISPATCH_QKV, False, D.RETURN_O), (D.DISPATCH_DO, True, D.RETURN_GRAD)):
+        for h in (0, 1):
+            for r, L in enumerate(layers):
+                L.dispatch(0, h, what, ios[r], s)
+        for h in (0, 1):
+            for L in layers:
+                L.compute(0, h, bwd, s)
+        for h in (0, 1):
+            for r, L in enumerate(layers):
+                L.ret(0, h, ret, ios[r], s)
+    for r, L in enumerate(layers):
+        L.finish(ios[r], s)
     torch.cuda.synchronize()
     out = {n: [bufs[r][n].float().cpu().numpy() for r in range(world)] for n in ("o", "lse", "dq", "dk", "dv")}
     launches = sum(L.launches for L in layers)

@@ -61,3 +61,40 @@ def test_lse_identity():
     for i in range(10):
         vis = s[i, : 6 + i + 1]
         assert abs(lse[0, i] - np.log(np.exp(vis).sum())) < 1e-5
+
+
+def test_backward_matches_finite_differences_of_the_forward():
+    """The oracle's backward is the gradient of its own forward: central
+    differences of L = sum(O * G) (accumulated in fp64 from the fp32 O) with
+    respect to random entries of Q, K and V, on two shards of one document
+    sharing its KV prefix plus a second document, GQA group 2."""
+    rng = np.random.default_rng(11)
+    hq, hkv = 2, 1
+    tasks = [(0, 23, 0, 23), (23, 17, 0, 40), (40, 9, 40, 9)]
+    rows = 49
+    q = rng.standard_normal((rows, hq, 128), dtype=np.float32)
+    k = rng.standard_normal((rows, hkv, 128), dtype=np.float32)
+    v = rng.standard_normal((rows, hkv, 128), dtype=np.float32)
+    g = rng.standard_normal((rows, hq, 128), dtype=np.float32)
+
+    def loss(q_, k_, v_):
+        o, _ = oracle.ca_forward(tasks, q_, k_, v_)
+        return float((o.astype(np.float64) * g).sum())
+
+    o, _ = oracle.ca_forward(tasks, q, k, v)
+    grads = dict(zip("qkv", oracle.ca_backward(tasks, q, k, v, o, g)))
+    h = 1e-2
+    worst = 0.0
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        for _ in range(12):
+            idx = tuple(int(rng.integers(0, s)) for s in x.shape)
+            xp, xm = x.copy(), x.copy()
+            xp[idx] += h
+            xm[idx] -= h
+            args_p = {"q": q, "k": k, "v": v, name: xp}
+            args_m = {"q": q, "k": k, "v": v, name: xm}
+            fd = (loss(args_p["q"], args_p["k"], args_p["v"]) - loss(args_m["q"], args_m["k"], args_m["v"])) / (2 * h)
+            an = float(grads[name][idx])
+            worst = max(worst, abs(fd - an) / (1e-1 + abs(an)))
+            assert abs(fd - an) <= 3e-3 + 2e-2 * abs(an), (name, idx, fd, an)
+    print("finite differences vs oracle backward, worst scaled error", worst)
