@@ -104,6 +104,18 @@ def run(args, metric, load_peaks, ClockSampler):
     ms_signal, _ = _timed(lambda: step(mode="signal"), n_side, comp)
     ms_serial, _ = _timed(lambda: step(mode="serial"), n_side, comp)
 
+    # CAD_TRACE=1: the phase timeline of one ping-pong step on every rank
+    traces = None
+    if os.environ.get("CAD_TRACE"):
+        layer.set_trace(True)
+        dist.barrier()
+        step()
+        torch.cuda.synchronize()
+        tr = layer.trace()
+        layer.set_trace(False)
+        traces = [None] * world
+        dist.all_gather_object(traces, tr)
+
     # NCCL transport (north_star's all-to-allv on a side stream), same
     # schedule and layers, CA grid leaving CAD_NCCL_RESERVE SMs to NCCL
     nccl = None
@@ -268,6 +280,9 @@ def run(args, metric, load_peaks, ClockSampler):
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if traces is not None:
+            out["trace_ranks"] = {"columns": ["phase", "layer", "half", "t_begin_ms", "t_ready_ms", "t_end_ms"],
+                                  "ranks": traces}
         print(json.dumps(out))
     layer.close()
     dist.barrier()

@@ -589,6 +589,29 @@ int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
 int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode,
                    void* stream);
 
+/* Timeline of the last cad_layer_step (tracing on): one record per phase,
+ * times in ms from the step's start on its compute stream. For FWD/BWD,
+ * t_ready is when the inputs had arrived (flags/events satisfied). */
+#define CAD_TRACE_DISPATCH_QKV 0
+#define CAD_TRACE_DISPATCH_DO 1
+#define CAD_TRACE_FWD 2
+#define CAD_TRACE_BWD 3
+#define CAD_TRACE_RETURN_O 4
+#define CAD_TRACE_RETURN_GRAD 5
+#define CAD_TRACE_FINISH 6
+typedef struct cad_trace_rec {
+  int32_t kind;
+  int32_t layer;
+  int32_t half;
+  int32_t pad_;
+  float t_begin;
+  float t_ready;
+  float t_end;
+  float pad2_;
+} cad_trace_rec;
+int cad_layer_ctx_set_trace(cad_layer_ctx* ctx, int32_t on);
+int cad_layer_ctx_trace(cad_layer_ctx* ctx, cad_trace_rec* recs, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -116,6 +116,11 @@ class cad_layer_ctx_info(C.Structure):
                 ("launches", i64)]
 
 
+class cad_trace_rec(C.Structure):
+    _fields_ = [("kind", i32), ("layer", i32), ("half", i32), ("pad_", i32), ("t_begin", f32),
+                ("t_ready", f32), ("t_end", f32), ("pad2_", f32)]
+
+
 class cad_layer_io(C.Structure):
     _fields_ = [("q", C.c_void_p), ("k", C.c_void_p), ("v", C.c_void_p), ("dout", C.c_void_p),
                 ("o", C.c_void_p), ("lse", C.c_void_p), ("dq", C.c_void_p), ("dk", C.c_void_p),
@@ -195,6 +200,8 @@ SIGNATURES = {
     "cad_return": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp]),
     "cad_layer_finish": (C.c_int, [vp, P(cad_layer_io), vp]),
     "cad_layer_step": (C.c_int, [vp, P(cad_layer_io), i32, vp]),
+    "cad_layer_ctx_set_trace": (C.c_int, [vp, i32]),
+    "cad_layer_ctx_trace": (C.c_int, [vp, P(cad_trace_rec), i64, P(i64)]),
 }
 
 _lib = None

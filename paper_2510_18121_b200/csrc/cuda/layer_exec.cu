@@ -503,21 +503,31 @@ struct cad_layer_ctx {
       cad_layer_ctx* c;
       ~Restore() { c->move = true; }
     } restore{this};
+    trace_reset(comp);
     cuda_check(cudaEventRecord(event(0), comp), "event");
     cuda_check(cudaStreamWaitEvent(comm, event(0), 0), "wait");
     begin(comm);
     auto disp = [&](int l, int h, int what) {
+      const int m0 = tmark(comm);
       dispatch(l, h, what, io, comm, comp);
+      trace_add(what == CAD_DISPATCH_QKV ? CAD_TRACE_DISPATCH_QKV : CAD_TRACE_DISPATCH_DO, l, h, m0, m0,
+                tmark(comm));
       cuda_check(cudaEventRecord(event(slot(l, h, what == CAD_DISPATCH_QKV ? 0 : 1)), comm), "event");
     };
     auto ca = [&](int l, int h, bool bwd) {
+      const int m0 = tmark(comp);
       cuda_check(cudaStreamWaitEvent(comp, event(slot(l, h, bwd ? 1 : 0)), 0), "wait");
-      compute(l, h, bwd, comp, true, run);
+      if (flagged()) await(bwd ? F_DO : F_QKV, h, bwd ? gb(l) : gl(l), comp);
+      const int m1 = tmark(comp);
+      compute(l, h, bwd, comp, false, run);
+      trace_add(bwd ? CAD_TRACE_BWD : CAD_TRACE_FWD, l, h, m0, m1, tmark(comp));
       cuda_check(cudaEventRecord(event(slot(l, h, bwd ? 3 : 2)), comp), "event");
     };
     auto back = [&](int l, int h, int what) {
       cuda_check(cudaStreamWaitEvent(comm, event(slot(l, h, what == CAD_RETURN_O ? 2 : 3)), 0), "wait");
+      const int m0 = tmark(comm);
       ret(l, h, what, io, comm, comp);
+      trace_add(what == CAD_RETURN_O ? CAD_TRACE_RETURN_O : CAD_TRACE_RETURN_GRAD, l, h, m0, m0, tmark(comm));
     };
     // forward: comm D(0,0) D(1,0) dO(.,L-1) | R(0,l) D(0,l+1) | R(1,l) D(1,l+1) ...
     //          comp       F(0,0)    F(1,0)      F(0,l+1)         F(1,l+1)
@@ -549,8 +559,40 @@ struct cad_layer_ctx {
         }
       }
     cuda_check(cudaEventRecord(event(1), comm), "event");
+    const int f0 = tmark(comp);
     cuda_check(cudaStreamWaitEvent(comp, event(1), 0), "wait");
+    const int f1 = tmark(comp);
     finish(io, comp);
+    trace_add(CAD_TRACE_FINISH, 0, 0, f0, f1, tmark(comp));
+  }
+
+  // ------------------------------------------------------------- tracing
+  // With tracing on, a step records timing events around every phase; the
+  // records of the last step are read back with cad_layer_ctx_trace.
+  bool tracing = false;
+  std::vector<cudaEvent_t> tev;  // timing events, [0] = step start
+  int tused = 0;
+  struct TraceRow {
+    int kind, layer, half, m0, m1, m2;
+  };
+  std::vector<TraceRow> trows;
+  void trace_reset(cudaStream_t s) {
+    trows.clear();
+    tused = 0;
+    if (tracing) tmark(s);
+  }
+  int tmark(cudaStream_t s) {
+    if (!tracing) return -1;
+    if (tused == static_cast<int>(tev.size())) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      tev.push_back(e);
+    }
+    cuda_check(cudaEventRecord(tev[static_cast<size_t>(tused)], s), "event");
+    return tused++;
+  }
+  void trace_add(int kind, int l, int h, int m0, int m1, int m2) {
+    if (tracing) trows.push_back({kind, l, h, m0, m1, m2});
   }
 
   ~cad_layer_ctx() {  // runs with the context's device current
@@ -568,6 +610,7 @@ struct cad_layer_ctx {
     cudaFree(xsend);
     cudaFree(xrecv);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (comm_stream) cudaStreamDestroy(comm_stream);
   }
 };
@@ -852,6 +895,32 @@ int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream) {
     ctx->need_ready();
     cad_dev::DeviceGuard dg(ctx->device);
     ctx->finish(io, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int cad_layer_ctx_set_trace(cad_layer_ctx* ctx, int32_t on) {
+  return cad::guarded([&] {
+    if (!ctx) throw cad::DomainError("null argument");
+    ctx->tracing = on != 0;
+  });
+}
+
+int cad_layer_ctx_trace(cad_layer_ctx* ctx, cad_trace_rec* recs, int64_t cap, int64_t* n) {
+  return cad::guarded([&] {
+    if (!ctx || !n) throw cad::DomainError("null argument");
+    cad_dev::DeviceGuard dg(ctx->device);
+    *n = static_cast<int64_t>(ctx->trows.size());
+    if (cap < *n || (*n > 0 && !recs)) throw cad::CapacityError("trace buffer too small");
+    if (*n > 0) cuda_check(cudaEventSynchronize(ctx->tev[ctx->tused - 1]), "trace sync");
+    auto at = [&](int m) {
+      float ms = 0.0f;
+      if (m >= 0) cuda_check(cudaEventElapsedTime(&ms, ctx->tev[0], ctx->tev[static_cast<size_t>(m)]), "elapsed");
+      return ms;
+    };
+    for (size_t i = 0; i < ctx->trows.size(); ++i) {
+      const auto& r = ctx->trows[i];
+      recs[i] = cad_trace_rec{r.kind, r.layer, r.half, 0, at(r.m0), at(r.m1), at(r.m2), 0.0f};
+    }
   });
 }
 

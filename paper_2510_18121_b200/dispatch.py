@@ -250,6 +250,23 @@ class DistCALayer:
     def finish(self, io, stream):
         check(lib().cad_layer_finish(self._h, C.byref(io), stream.cuda_stream))
 
+    def set_trace(self, on: bool) -> None:
+        check(lib().cad_layer_ctx_set_trace(self._h, int(on)))
+
+    TRACE_KINDS = ("D", "dO", "F", "B", "R", "G", "finish")
+
+    def trace(self):
+        """Phases of the last traced step: (kind, layer, half, t_begin,
+        t_ready, t_end) in ms from the step's start."""
+        n = N.i64()
+        rc = lib().cad_layer_ctx_trace(self._h, None, 0, C.byref(n))
+        if rc not in (0, N.CAD_ERR_CAPACITY):
+            check(rc)
+        recs = (N.cad_trace_rec * max(1, n.value))()
+        check(lib().cad_layer_ctx_trace(self._h, recs, n.value, C.byref(n)))
+        return [(self.TRACE_KINDS[r.kind], r.layer, r.half, round(r.t_begin, 3), round(r.t_ready, 3),
+                 round(r.t_end, 3)) for r in recs[:n.value]]
+
     def close(self):
         if getattr(self, "_h", None):
             with torch.cuda.device(self.dev):
