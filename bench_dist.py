@@ -102,6 +102,7 @@ def run(args, metric, load_peaks, ClockSampler):
     ms_compute, my_compute = _timed(lambda: step(mode="compute"), n_side, comp)
     ms_comm, _ = _timed(lambda: step(mode="comm"), n_side, comp)
     ms_signal, _ = _timed(lambda: step(mode="signal"), n_side, comp)
+    ms_comm_local, _ = _timed(lambda: step(mode="comm_local"), n_side, comp)
     ms_serial, _ = _timed(lambda: step(mode="serial"), n_side, comp)
 
     # CAD_TRACE=1: the phase timeline of one ping-pong step on every rank
@@ -230,9 +231,15 @@ def run(args, metric, load_peaks, ClockSampler):
         total_pairs = allst[:, 0].sum()
         flops = 14.0 * 128 * shape.h_q * total_pairs * layers
         value = flops / ms / 1e9
-        # hidden = 1 - (T_pingpong - T_signal) / T_comm_only (the
-        # reference's signal/ping-pong modes, P/tests/acceptance.cpp:272-290)
-        hidden = max(0.0, min(1.0, 1.0 - (ms - ms_signal) / ms_comm)) if ms_comm > 0 else None
+        # hidden = 1 - (T_pingpong - T_signal) / T_wire (the
+        # reference's signal/ping-pong modes, P/tests/acceptance.cpp:272-290):
+        # signal = the same step with every transfer to a peer shrunk to its
+        # flag; T_wire = the peer transfers alone (comm-only minus comm-only
+        # without them). hidden_all also charges the rank's own row copies,
+        # the dK/dV reduction and the kernels' slowdown under concurrent
+        # copies against all data movement: 1 - (T_pp - T_compute) / T_comm.
+        wire_ms = ms_comm - ms_comm_local
+        hidden = max(0.0, min(1.0, 1.0 - (ms - ms_signal) / wire_ms)) if wire_ms > 0 else None
         hidden_vs_compute = max(0.0, min(1.0, 1.0 - (ms - ms_compute) / ms_comm)) if ms_comm > 0 else None
         naive_pairs = []
         for r in range(world):
@@ -259,8 +266,9 @@ def run(args, metric, load_peaks, ClockSampler):
                           "max_over_mean_ca_time": float(allst[:, 1].max() / allst[:, 1].mean()),
                           "naive_max_over_mean_pairs": max(naive_pairs) / (sum(naive_pairs) / world)},
             "comm": {"ms_compute_only": ms_compute, "ms_signal": ms_signal, "ms_comm_only": ms_comm,
+                     "ms_comm_local_only": ms_comm_local, "ms_wire": wire_ms,
                      "ms_serial": ms_serial, "ms_pingpong": ms, "hidden_fraction": hidden,
-                     "hidden_fraction_vs_compute_only": hidden_vs_compute,
+                     "hidden_fraction_all_movement": hidden_vs_compute,
                      "nccl": nccl,
                      "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
                      "nvlink_gbs_per_gpu": float(allst[:, 2].max()) / (ms_comm / 1e3) / 1e9 if ms_comm else None,

@@ -515,8 +515,8 @@ typedef struct cad_layer_ctx_info {
  * order of the rank's home items): inputs q/dout [home_rows][h_q][d], k/v
  * [home_rows][h_kv][d] bf16; outputs o/dq bf16 and lse [h_q][home_rows] fp32
  * (these three must be the buffers given to cad_layer_ctx_bind_outputs),
- * dk/dv bf16 (may be NULL) and their fp32 sums dk_acc/dv_acc
- * [home_rows][h_kv][d] (NULL: context-owned). */
+ * dk/dv bf16 and/or their fp32 sums dk_acc/dv_acc [home_rows][h_kv][d]
+ * (each written when non-NULL). */
 typedef struct cad_layer_io {
   const void* q;
   const void* k;
@@ -572,8 +572,9 @@ int cad_layer_compute(cad_layer_ctx* ctx, int32_t layer, int32_t half,
                       int32_t backward, void* stream);
 int cad_return(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
                const cad_layer_io* io, void* stream);
-/* Waits for every return addressed to this rank, sums the dK/dV partials into
- * dk_acc/dv_acc (fp32, zeroed first), writes dk/dv (bf16) if given. */
+/* Waits for every return addressed to this rank and sums, per home KV row,
+ * the dK/dV partials of every server that used it (fp32, no atomics) into
+ * dk/dv (bf16) and/or dk_acc/dv_acc (fp32). */
 int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
 
 /* One whole step (all layers, forward + backward) on `stream` (compute) and
@@ -583,9 +584,13 @@ int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
 #define CAD_STEP_SERIAL 1   /* everything on `stream`, no overlap */
 #define CAD_STEP_COMPUTE 2  /* CA kernels only (server buffers as resident) */
 #define CAD_STEP_COMM 3     /* exchanges only, no CA kernels */
-#define CAD_STEP_SIGNAL 4   /* ping-pong with every flag but no row copies
-                               (the reference's signal mode, sim.hpp:14-18;
-                               LOCAL/IPC only) */
+#define CAD_STEP_SIGNAL 4   /* ping-pong with every flag, the rank's own
+                               rows and the dK/dV reduction, but every
+                               transfer to a peer shrunk to its flag (the
+                               reference's signal mode, sim.hpp:14-18;
+                               IPC only) */
+#define CAD_STEP_COMM_LOCAL 5 /* COMM without the transfers to peers: the
+                                 rank's own rows and the reduction only */
 int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode,
                    void* stream);
 

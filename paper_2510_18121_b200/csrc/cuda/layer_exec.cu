@@ -31,6 +31,7 @@
 // g0: forward of layer l -> g0+1+l, backward of layer l -> g0+2L-l, done ->
 // g0+2L, so every wait is ">= value" and a later signal never under-shoots.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -199,6 +200,52 @@ struct Peer {
   Layout layout;
 };
 
+// dK/dV at the owner: every home KV row gathers its partials -- one per
+// (server, half, layer) that used it, listed in CSR form (off[row] ..
+// off[row+1]) as staging rows of a half -- sums them in fp32 and writes bf16
+// (and fp32 when asked). One warp per row, 16-byte loads; each partial is read
+// once and each output written once: no memset, no atomics.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ ent,
+                                                              const uint4* const* __restrict__ src,  // [layer][half]
+                                                              int n_layers, int64_t rows, int chunks,
+                                                              uint4* __restrict__ out_bf16,
+                                                              float4* __restrict__ out_f32) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = off[row], e1 = off[row + 1];
+  for (int c = lane; c < chunks; c += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t e = e0; e < e1; ++e) {
+      const int32_t v = ent[e];
+      const int half = v & 1;
+      const int64_t srow = v >> 1;
+      for (int l = 0; l < n_layers; ++l) {
+        const uint4 x = src[l * 2 + half][srow * chunks + c];
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(b[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
+    }
+    if (out_bf16) {
+      uint4 o;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      out_bf16[row * chunks + c] = o;
+    }
+    if (out_f32) {
+      out_f32[(row * chunks + c) * 2] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      out_f32[(row * chunks + c) * 2 + 1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
 template <class T>
 T* dev_copy(const std::vector<T>& v) {
   T* d = nullptr;
@@ -229,7 +276,9 @@ struct cad_layer_ctx {
   std::vector<size_t> run_off[2][4];  // per peer: first run (W + 1 entries)
   i64* d_send_idx[2][4] = {};
   i64* d_recv_idx[2][4] = {};
-  float* acc_own[2] = {nullptr, nullptr};  // dK/dV fp32 sums when the caller gives none
+  int64_t* d_red_off = nullptr;  // dK/dV reduction CSR over home rows
+  int32_t* d_red_ent = nullptr;  // (staging row << 1) | half
+  const uint4** d_red_src[2] = {nullptr, nullptr};  // dK, dV staging bases [layer][half]
   void* o_home = nullptr;
   float* lse_home = nullptr;
   void* dq_home = nullptr;
@@ -242,7 +291,9 @@ struct cad_layer_ctx {
   std::vector<cudaEvent_t> ev;
   uint32_t gen = 0, g0 = 0;
   i64 launches = 0;
-  bool move = true;  // false: signal mode (flags without row copies)
+  bool move = true;         // false: no row copies at all (NCCL: no exchange)
+  bool move_remote = true;  // false: signal mode -- this rank's own rows still
+                            // move, the transfers to peers shrink to their flags
 
   // ------------------------------------------------------------- helpers
   Bufs b(int l, int h) const { return layout.b[static_cast<size_t>(l)][static_cast<size_t>(h)]; }
@@ -280,7 +331,7 @@ struct cad_layer_ctx {
     if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
-      if (a == e) continue;
+      if (a == e || (p != me && !move_remote)) continue;
       ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes,
                        p == me ? local : s),
          "cad_copy_runs");
@@ -290,7 +341,7 @@ struct cad_layer_ctx {
     if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][kXO][static_cast<size_t>(p)], e = run_off[h][kXO][static_cast<size_t>(p) + 1];
-      if (a == e) continue;
+      if (a == e || (p != me && !move_remote)) continue;
       const Peer& P = peer[static_cast<size_t>(p)];
       ok(cad_copy_runs_cols(runs[h][kXO].data() + a, static_cast<i64>(e - a), src, src_rows, P.lse, P.home_rows,
                             static_cast<int32_t>(hq), p == me ? local : s),
@@ -442,30 +493,17 @@ struct cad_layer_ctx {
         await(F_O, h, gl(NL - 1), s);
         await(F_G, h, gb(0), s);
       }
-    float* dk_acc = io->dk_acc ? io->dk_acc : acc_own[0];
-    float* dv_acc = io->dv_acc ? io->dv_acc : acc_own[1];
-    const i64 elems = mine.home_rows * hkv * d;
-    if (elems > 0) {
-      cuda_check(cudaMemsetAsync(dk_acc, 0, static_cast<size_t>(elems) * 4, s), "memset dk_acc");
-      cuda_check(cudaMemsetAsync(dv_acc, 0, static_cast<size_t>(elems) * 4, s), "memset dv_acc");
-    }
-    if (move)
-      for (int l = NL - 1; l >= 0; --l)
-        for (int h = 0; h < 2; ++h) {
-          const i64 n = mine.half[h].x[kXKR].n_recv();
-          if (!n) continue;
-          const Bufs& B = b(l, h);
-          ok(cad_scatter_add_bf16(at(B.sdk), d_recv_idx[h][kXKR], n, hkv * d, dk_acc, s), "scatter_add dk");
-          ok(cad_scatter_add_bf16(at(B.sdv), d_recv_idx[h][kXKR], n, hkv * d, dv_acc, s), "scatter_add dv");
-          launches += 2;
-        }
-    if (elems > 0 && io->dk) {
-      ok(cad_f32_to_bf16(dk_acc, elems, io->dk, s), "f32_to_bf16 dk");
-      ++launches;
-    }
-    if (elems > 0 && io->dv) {
-      ok(cad_f32_to_bf16(dv_acc, elems, io->dv, s), "f32_to_bf16 dv");
-      ++launches;
+    const i64 rows = mine.home_rows;
+    const int chunks = static_cast<int>(hkv * d / 8);
+    if (rows > 0 && (io->dk || io->dk_acc || io->dv || io->dv_acc)) {
+      const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+      const int n_layers = move ? NL : 0;
+      reduce_partials_kernel<<<blocks, 256, 0, s>>>(d_red_off, d_red_ent, d_red_src[0], n_layers, rows, chunks,
+                                                    static_cast<uint4*>(io->dk), reinterpret_cast<float4*>(io->dk_acc));
+      reduce_partials_kernel<<<blocks, 256, 0, s>>>(d_red_off, d_red_ent, d_red_src[1], n_layers, rows, chunks,
+                                                    static_cast<uint4*>(io->dv), reinterpret_cast<float4*>(io->dv_acc));
+      cuda_check(cudaGetLastError(), "reduce_partials launch");
+      launches += 2;
     }
     if (flagged()) signal(F_DONE, 0, gdone(), s);
   }
@@ -493,15 +531,16 @@ struct cad_layer_ctx {
         for (int h = 0; h < 2; ++h) compute(l, h, true, comp, false, true);
       return;
     }
-    if (mode == CAD_STEP_SIGNAL && !flagged()) throw cad::ConfigError("signal mode needs the LOCAL or IPC transport");
-    if (mode < CAD_STEP_PINGPONG || mode > CAD_STEP_SIGNAL) throw cad::DomainError("unknown step mode");
+    if ((mode == CAD_STEP_SIGNAL || mode == CAD_STEP_COMM_LOCAL) && !flagged())
+      throw cad::ConfigError("signal modes need the LOCAL or IPC transport");
+    if (mode < CAD_STEP_PINGPONG || mode > CAD_STEP_COMM_LOCAL) throw cad::DomainError("unknown step mode");
     check_io(io, true);
-    const bool run = mode != CAD_STEP_COMM;
-    move = mode != CAD_STEP_SIGNAL;
+    const bool run = mode != CAD_STEP_COMM && mode != CAD_STEP_COMM_LOCAL;
+    move_remote = mode != CAD_STEP_SIGNAL && mode != CAD_STEP_COMM_LOCAL;
     cudaStream_t comm = mode == CAD_STEP_SERIAL ? comp : comm_stream;
     struct Restore {
       cad_layer_ctx* c;
-      ~Restore() { c->move = true; }
+      ~Restore() { c->move_remote = true; }
     } restore{this};
     trace_reset(comp);
     cuda_check(cudaEventRecord(event(0), comp), "event");
@@ -604,9 +643,11 @@ struct cad_layer_ctx {
         cudaFree(d_send_idx[h][x]);
         cudaFree(d_recv_idx[h][x]);
       }
-      cudaFree(acc_own[h]);
+      cudaFree(d_red_src[h]);
     }
     cudaFree(arena);
+    cudaFree(d_red_off);
+    cudaFree(d_red_ent);
     cudaFree(xsend);
     cudaFree(xrecv);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -711,8 +752,29 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&C->arena), C->layout.total), "cudaMalloc(server buffers)");
     C->flags = C->at<int32_t>(C->layout.flags);
     cuda_check(cudaMemset(C->flags, 0, static_cast<size_t>(4) * 2 * kKinds * C->W), "memset flags");
-    const size_t acc = static_cast<size_t>(std::max<i64>(1, C->mine.home_rows * C->hkv * C->d)) * 4;
-    for (int i = 0; i < 2; ++i) cuda_check(cudaMalloc(reinterpret_cast<void**>(&C->acc_own[i]), acc), "cudaMalloc(acc)");
+    {  // dK/dV reduction CSR: home row -> (half, staging row) of every partial
+      std::vector<std::vector<int32_t>> per(static_cast<size_t>(std::max<i64>(1, C->mine.home_rows)));
+      for (int h = 0; h < 2; ++h) {
+        const auto& ri = C->mine.half[h].x[kXKR].recv_idx;
+        if (static_cast<i64>(ri.size()) >= (i64(1) << 30)) throw cad::ConfigError("too many partial rows");
+        for (size_t j = 0; j < ri.size(); ++j)
+          per[static_cast<size_t>(ri[j])].push_back(static_cast<int32_t>(j) << 1 | h);
+      }
+      std::vector<int64_t> off(1, 0);
+      std::vector<int32_t> ent;
+      for (const auto& v : per) {
+        ent.insert(ent.end(), v.begin(), v.end());
+        off.push_back(static_cast<int64_t>(ent.size()));
+      }
+      C->d_red_off = dev_copy(off);
+      C->d_red_ent = dev_copy(ent);
+      for (int t = 0; t < 2; ++t) {
+        std::vector<const uint4*> src;
+        for (int l = 0; l < C->NL; ++l)
+          for (int h = 0; h < 2; ++h) src.push_back(C->at<const uint4>(t == 0 ? C->b(l, h).sdk : C->b(l, h).sdv));
+        C->d_red_src[t] = dev_copy(src);
+      }
+    }
     if (cfg->transport == CAD_TRANSPORT_NCCL) {
       C->xbytes = xmax;
       cuda_check(cudaMalloc(&C->xsend, xmax), "cudaMalloc(send)");

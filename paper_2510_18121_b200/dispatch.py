@@ -141,7 +141,7 @@ class Comm:
 
 
 TRANSPORTS = {"local": 0, "ipc": 1, "ce": 1, "nccl": 2}
-MODES = {"pingpong": 0, "serial": 1, "compute": 2, "comm": 3, "signal": 4}
+MODES = {"pingpong": 0, "serial": 1, "compute": 2, "comm": 3, "signal": 4, "comm_local": 5}
 DISPATCH_QKV, DISPATCH_DO = 0, 1
 RETURN_O, RETURN_GRAD = 0, 1
 
