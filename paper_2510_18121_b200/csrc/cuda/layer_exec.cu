@@ -202,7 +202,8 @@ struct Peer {
 
 // dK/dV at the owner: every home KV row gathers its partials -- one per
 // (server, half, layer) that used it, listed in CSR form (off[row] ..
-// off[row+1]) as staging rows of a half -- sums them in fp32 and writes bf16
+// off[row+1]) as a row of a half's staging (peers' partials) or of its server
+// dK/dV buffer (this rank's own) -- sums them in fp32 and writes bf16
 // (and fp32 when asked). One warp per row, 16-byte loads; each partial is read
 // once and each output written once: no memset, no atomics.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const int64_t* __restrict__ off,
@@ -219,10 +220,10 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const int64_t* __r
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int64_t e = e0; e < e1; ++e) {
       const int32_t v = ent[e];
-      const int half = v & 1;
-      const int64_t srow = v >> 1;
+      const int slot = v & 3;  // own (server buffer) << 1 | half
+      const int64_t srow = v >> 2;
       for (int l = 0; l < n_layers; ++l) {
-        const uint4 x = src[l * 2 + half][srow * chunks + c];
+        const uint4 x = src[l * 4 + slot][srow * chunks + c];
         const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&x);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -242,6 +243,35 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const int64_t* __r
     if (out_f32) {
       out_f32[(row * chunks + c) * 2] = make_float4(acc[0], acc[1], acc[2], acc[3]);
       out_f32[(row * chunks + c) * 2 + 1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
+// This rank's own rows (tasks it serves itself) move between its home and
+// server buffers in ONE launch per exchange: chunks of <= kChunkRows rows
+// (src_row, dst_row, n) dealt to CTAs grid-stride, 16-byte vectors. One
+// cudaMemcpyAsync per run instead costs the host microseconds per run --
+// thousands per step with short documents -- and the GPU idles behind it.
+constexpr int kChunkRows = 32;
+__global__ void __launch_bounds__(256) copy_row_chunks_kernel(const int64_t* __restrict__ chunks, int64_t n_chunks,
+                                                              const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                              int64_t row_vec) {
+  for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int64_t sr = chunks[3 * c], dr = chunks[3 * c + 1], n = chunks[3 * c + 2];
+    const uint4* s = src + sr * row_vec;
+    uint4* d = dst + dr * row_vec;
+    for (int64_t i = threadIdx.x; i < n * row_vec; i += blockDim.x) d[i] = s[i];
+  }
+}
+// The same for the [heads][rows] fp32 LSE.
+__global__ void __launch_bounds__(256) copy_col_chunks_kernel(const int64_t* __restrict__ chunks, int64_t n_chunks,
+                                                              const float* __restrict__ src, int64_t src_rows,
+                                                              float* __restrict__ dst, int64_t dst_rows, int heads) {
+  for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int64_t sr = chunks[3 * c], dr = chunks[3 * c + 1], n = chunks[3 * c + 2];
+    for (int64_t i = threadIdx.x; i < n * heads; i += blockDim.x) {
+      const int64_t h = i / n, j = i - h * n;
+      dst[h * dst_rows + dr + j] = src[h * src_rows + sr + j];
     }
   }
 }
@@ -274,11 +304,13 @@ struct cad_layer_ctx {
   std::vector<void*> opened;  // IPC mappings to close
   std::vector<cad_run> runs[2][4];  // per (half, xfer): runs of all peers, grouped by peer
   std::vector<size_t> run_off[2][4];  // per peer: first run (W + 1 entries)
+  int64_t* d_local_chunks[2][4] = {};  // this rank's own rows: device chunk lists
+  int64_t n_local_chunks[2][4] = {};
   i64* d_send_idx[2][4] = {};
   i64* d_recv_idx[2][4] = {};
   int64_t* d_red_off = nullptr;  // dK/dV reduction CSR over home rows
-  int32_t* d_red_ent = nullptr;  // (staging row << 1) | half
-  const uint4** d_red_src[2] = {nullptr, nullptr};  // dK, dV staging bases [layer][half]
+  int32_t* d_red_ent = nullptr;  // (row << 2) | (own << 1) | half
+  const uint4** d_red_src[2] = {nullptr, nullptr};  // dK, dV bases [layer][own][half]
   void* o_home = nullptr;
   float* lse_home = nullptr;
   void* dq_home = nullptr;
@@ -327,24 +359,45 @@ struct cad_layer_ctx {
   // local copy overlapping a CA kernel crawls and would hold up the remote
   // pushes queued behind it)
   template <class DstOf>
-  void push(int h, int x, const void* src, i64 row_bytes, DstOf dst_of, cudaStream_t s, cudaStream_t local) const {
+  void push(int h, int x, const void* src, i64 row_bytes, DstOf dst_of, cudaStream_t s, cudaStream_t local) {
     if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
-      if (a == e || (p != me && !move_remote)) continue;
-      ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes,
-                       p == me ? local : s),
+      if (a == e) continue;
+      if (p == me) {
+        // own dK/dV partials stay in the server buffers (the reduction reads them there)
+        if (x == kXKR) continue;
+        const int64_t n = n_local_chunks[h][x];
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n, 148 * 4));
+        copy_row_chunks_kernel<<<grid, 256, 0, local>>>(d_local_chunks[h][x], n, static_cast<const uint4*>(src),
+                                                        static_cast<uint4*>(dst_of(p)), row_bytes / 16);
+        cuda_check(cudaGetLastError(), "copy_row_chunks launch");
+        ++launches;
+        continue;
+      }
+      if (!move_remote) continue;
+      ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes, s),
          "cad_copy_runs");
     }
   }
-  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) const {
+  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) {
     if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][kXO][static_cast<size_t>(p)], e = run_off[h][kXO][static_cast<size_t>(p) + 1];
-      if (a == e || (p != me && !move_remote)) continue;
+      if (a == e) continue;
       const Peer& P = peer[static_cast<size_t>(p)];
+      if (p == me) {
+        const int64_t n = n_local_chunks[h][kXO];
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n, 148 * 4));
+        copy_col_chunks_kernel<<<grid, 256, 0, local>>>(d_local_chunks[h][kXO], n, src, src_rows, P.lse,
+                                                        P.home_rows, static_cast<int>(hq));
+        cuda_check(cudaGetLastError(), "copy_col_chunks launch");
+        ++launches;
+        continue;
+      }
+      if (!move_remote) continue;
       ok(cad_copy_runs_cols(runs[h][kXO].data() + a, static_cast<i64>(e - a), src, src_rows, P.lse, P.home_rows,
-                            static_cast<int32_t>(hq), p == me ? local : s),
+                            static_cast<int32_t>(hq), s),
          "cad_copy_runs_cols");
     }
   }
@@ -642,6 +695,7 @@ struct cad_layer_ctx {
       for (int x = 0; x < 4; ++x) {
         cudaFree(d_send_idx[h][x]);
         cudaFree(d_recv_idx[h][x]);
+        cudaFree(d_local_chunks[h][x]);
       }
       cudaFree(d_red_src[h]);
     }
@@ -676,6 +730,12 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     C->cfg = *cfg;
     cuda_check(cudaGetDevice(&C->device), "cudaGetDevice");
     cad_dev::preload_kernels();
+    for (const void* f : {reinterpret_cast<const void*>(copy_row_chunks_kernel),
+                          reinterpret_cast<const void*>(copy_col_chunks_kernel),
+                          reinterpret_cast<const void*>(reduce_partials_kernel)}) {
+      cudaFuncAttributes a;  // loaded now, not mid-step (see preload_kernels)
+      cuda_check(cudaFuncGetAttributes(&a, f), "load executor kernels");
+    }
     C->W = cfg->world;
     C->me = cfg->rank;
     C->NL = cfg->layers;
@@ -717,8 +777,28 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
           R.insert(R.end(), rr.begin(), rr.end());
           off.push_back(R.size());
           so += n;
+          if (p == C->me) {
+            std::vector<int64_t> ch;
+            for (const cad_run& r : rr)
+              for (i64 a = 0; a < r.n_rows; a += kChunkRows) {
+                ch.push_back(r.src_row + a);
+                ch.push_back(r.dst_row + a);
+                ch.push_back(std::min<i64>(kChunkRows, r.n_rows - a));
+              }
+            C->n_local_chunks[h][x] = static_cast<int64_t>(ch.size() / 3);
+            C->d_local_chunks[h][x] = dev_copy(ch);
+          }
         }
       }
+    // own dK/dV partial rows: server row (in my KV_RET send list to myself) of
+    // the j-th staging row I receive from myself
+    std::vector<i64> own_src[2];
+    for (int h = 0; h < 2; ++h) {
+      const XferRows& M = C->mine.half[h].x[kXKR];
+      i64 so = 0;
+      for (int p = 0; p < C->me; ++p) so += M.send_counts[static_cast<size_t>(p)];
+      own_src[h].assign(M.send_idx.begin() + so, M.send_idx.begin() + so + M.send_counts[static_cast<size_t>(C->me)]);
+    }
     all.clear();
     // server CA plans and workspaces
     size_t xmax = 16;
@@ -755,10 +835,19 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     {  // dK/dV reduction CSR: home row -> (half, staging row) of every partial
       std::vector<std::vector<int32_t>> per(static_cast<size_t>(std::max<i64>(1, C->mine.home_rows)));
       for (int h = 0; h < 2; ++h) {
-        const auto& ri = C->mine.half[h].x[kXKR].recv_idx;
-        if (static_cast<i64>(ri.size()) >= (i64(1) << 30)) throw cad::ConfigError("too many partial rows");
-        for (size_t j = 0; j < ri.size(); ++j)
-          per[static_cast<size_t>(ri[j])].push_back(static_cast<int32_t>(j) << 1 | h);
+        const XferRows& X = C->mine.half[h].x[kXKR];
+        const auto& ri = X.recv_idx;
+        if (static_cast<i64>(ri.size()) >= (i64(1) << 29) || C->mine.half[h].kv_rows >= (i64(1) << 29))
+          throw cad::ConfigError("too many partial rows");
+        i64 own0 = 0;
+        for (int p = 0; p < C->me; ++p) own0 += X.recv_counts[static_cast<size_t>(p)];
+        const i64 own1 = own0 + X.recv_counts[static_cast<size_t>(C->me)];
+        for (size_t j = 0; j < ri.size(); ++j) {
+          const i64 jj = static_cast<i64>(j);
+          const bool own = jj >= own0 && jj < own1;  // my own partial: read in my server buffer
+          const i64 row = own ? own_src[h][static_cast<size_t>(jj - own0)] : jj;
+          per[static_cast<size_t>(ri[j])].push_back(static_cast<int32_t>(row << 2 | (own ? 2 : 0) | h));
+        }
       }
       std::vector<int64_t> off(1, 0);
       std::vector<int32_t> ent;
@@ -771,7 +860,11 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
       for (int t = 0; t < 2; ++t) {
         std::vector<const uint4*> src;
         for (int l = 0; l < C->NL; ++l)
-          for (int h = 0; h < 2; ++h) src.push_back(C->at<const uint4>(t == 0 ? C->b(l, h).sdk : C->b(l, h).sdv));
+          for (int own = 0; own < 2; ++own)
+            for (int h = 0; h < 2; ++h) {
+              const Bufs& B = C->b(l, h);
+              src.push_back(C->at<const uint4>(own ? (t == 0 ? B.dk : B.dv) : (t == 0 ? B.sdk : B.sdv)));
+            }
         C->d_red_src[t] = dev_copy(src);
       }
     }
