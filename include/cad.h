@@ -245,6 +245,20 @@ int cad_plan_server(const cad_plan* plan, int64_t server, cad_server_load* load,
 int cad_plan_to_text(const cad_plan* plan, char* buf, size_t cap, size_t* needed);
 void cad_plan_free(cad_plan* plan);
 
+/* Pipeline tick table of simulate_pp_iteration (P/src/sim.cpp:297-353):
+ * out[tick * n_stages + stage] for n_ticks ticks (two-call: out may be NULL
+ * with cap 0 to learn *n_ticks; CAD_ERR_CAPACITY then). Errors as the
+ * reference: n_stages < 1, n_microbatches < n_stages -> CAD_ERR_CONFIG. */
+#define CAD_PP_1F1B 0       /* PPSchedule::vanilla_1f1b */
+#define CAD_PP_PHASE_SYNC 1 /* PPSchedule::cad_phase_sync */
+typedef struct cad_tick_work {
+  int32_t active;
+  int32_t backward;
+  int64_t microbatch;
+} cad_tick_work;
+int cad_pp_tick_table(int64_t n_microbatches, int64_t n_stages, int32_t kind,
+                      cad_tick_work* out, int64_t cap, int64_t* n_ticks);
+
 /* device_plans_from_schedule (served/sent + assign_halves),
  * P/src/sim.cpp:34-46,129-157 */
 int cad_device_plan(const cad_plan* plan, int32_t device,
@@ -559,9 +573,21 @@ int cad_layer_ctx_destroy(cad_layer_ctx* ctx);
  * go to one stream. */
 #define CAD_DISPATCH_QKV 0 /* Q, K, V rows: home -> servers (forward)  */
 #define CAD_DISPATCH_DO 1  /* dO rows: home -> servers (backward)      */
+#define CAD_DISPATCH_FWD_STATE 2 /* O rows + LSE: home -> servers, for a
+                                    backward whose forward ran under another
+                                    plan (a pipeline tick, sim.cpp:326-353);
+                                    issue before the DO dispatch */
 #define CAD_RETURN_O 0     /* O rows + LSE: servers -> home            */
 #define CAD_RETURN_GRAD 1  /* dQ rows -> home, dK/dV partials -> owners */
 int cad_layer_begin(cad_layer_ctx* ctx, void* stream);
+/* Passes of a step: forward and backward (the default), or one of them (a
+ * pipeline tick runs one pass per tick; layers == 1). A forward-only step
+ * ends once the O/LSE returns arrived; a backward-only step dispatches Q/K/V,
+ * the forward state (O, LSE) and dO, and sums the dK/dV partials. */
+#define CAD_PASS_FWD 1
+#define CAD_PASS_BWD 2
+#define CAD_PASS_BOTH 3
+int cad_layer_begin_ex(cad_layer_ctx* ctx, int32_t passes, void* stream);
 int cad_dispatch(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what,
                  const cad_layer_io* io, void* stream);
 /* Same, with this rank's own rows (tasks it serves itself) copied on
@@ -593,6 +619,8 @@ int cad_layer_finish(cad_layer_ctx* ctx, const cad_layer_io* io, void* stream);
                                  rank's own rows and the reduction only */
 int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode,
                    void* stream);
+int cad_layer_step_ex(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode,
+                      int32_t passes, void* stream);
 
 /* Timeline of the last cad_layer_step (tracing on): one record per phase,
  * times in ms from the step's start on its compute stream. For FWD/BWD,

@@ -60,6 +60,9 @@ def ref_lib() -> C.CDLL:
             "ref_plan_free": (None, [vp]),
             "ref_schedule_seconds": (N.f64, [P(N.cad_item), N.i64, N.i64, P(N.cad_sched_cfg), N.i64]),
             "ref_grid_lookup": (N.f64, [C.c_char_p, N.f64, N.f64, N.i64, N.i64, N.i64]),
+            "ref_pp_iteration": (C.c_int, [P(N.cad_item), P(N.i64), N.i64, P(N.i64), N.i64, N.i64, C.c_int32,
+                                           P(N.cad_sched_cfg), P(N.i64), P(N.i64), P(C.c_int32), N.i64,
+                                           P(N.i64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(h, name)

@@ -315,4 +315,51 @@ double ref_schedule_seconds(const cad_item* items, int64_t n, int64_t n_servers,
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// simulate_pp_iteration (P/src/sim.cpp:297-485) on microbatches given as
+// items (mb_of[i] = microbatch of item i, tokens[m] = its tokens), an
+// 8B-like model with num_layers = stages (one layer per stage, so the wire
+// bytes stay integral) and the test suite's 8-GPU cluster shape: the tick
+// count, the total wire bytes, and per stage the kinds of its events
+// (0 forward, 1 backward; 1F1B) in time order.
+int ref_pp_iteration(const cad_item* items, const int64_t* mb_of, int64_t n_items, const int64_t* tokens,
+                     int64_t M, int64_t S, int32_t kind, const cad_sched_cfg* cfg, int64_t* ticks,
+                     int64_t* wire_bytes, int32_t* ev_kinds, int64_t ev_cap, int64_t* ev_count) {
+  return guard([&] {
+    std::vector<cadsim::Microbatch> mbs(static_cast<std::size_t>(M));
+    for (int64_t m = 0; m < M; ++m) mbs[static_cast<std::size_t>(m)].tokens = tokens[m];
+    for (int64_t i = 0; i < n_items; ++i) mbs[static_cast<std::size_t>(mb_of[i])].items.push_back(to_ref(items[i]));
+    cadsim::ModelConfig model;
+    model.num_layers = S;
+    model.hidden = 4096;
+    model.kv_hidden = 1024;
+    model.ffn_intermediate = 14336;
+    model.head_dim = 128;
+    model.num_heads = 32;
+    model.gqa_groups = 8;
+    model = cadsim::derive_sizes(model);
+    cadsim::ClusterConfig cluster;
+    cluster.num_gpus = S;
+    cluster.dp = S;
+    cluster.interconnect_bandwidth = 50.0 * (1ull << 30);
+    cluster.peak_flops = 990e12;
+    cluster.tile_size = 128;
+    const auto coeff = cadsim::derive_coefficients(model);
+    const auto grid = cadsim::synth_grid(model, cluster, 1 << 16);
+    cadsim::SimConfig sim;
+    sim.record_events = true;
+    const auto rep = cadsim::simulate_pp_iteration(
+        mbs, S, kind == CAD_PP_1F1B ? cadsim::PPSchedule::vanilla_1f1b : cadsim::PPSchedule::cad_phase_sync, model,
+        cluster, coeff, grid, sim, to_ref(*cfg));
+    *ticks = rep.ticks;
+    *wire_bytes = rep.total_wire_bytes;
+    for (int64_t s = 0; s < S; ++s) {
+      const auto& ev = rep.per_device[static_cast<std::size_t>(s)].events;
+      ev_count[s] = static_cast<int64_t>(ev.size());
+      for (std::size_t e = 0; e < ev.size() && static_cast<int64_t>(e) < ev_cap; ++e)
+        ev_kinds[s * ev_cap + static_cast<int64_t>(e)] =
+            (ev[e].kind == "backward" || ev[e].kind == "tick_backward") ? 1 : 0;
+    }
+  });
+}
+
 }  // extern "C"

@@ -104,6 +104,10 @@ class cad_run(C.Structure):
     _fields_ = [("src_row", i64), ("dst_row", i64), ("n_rows", i64)]
 
 
+class cad_tick_work(C.Structure):
+    _fields_ = [("active", i32), ("backward", i32), ("microbatch", i64)]
+
+
 class cad_layer_cfg(C.Structure):
     _fields_ = [("rank", i32), ("world", i32), ("h_q", i32), ("h_kv", i32), ("head_dim", i32),
                 ("softmax_scale", f32), ("transport", i32), ("layers", i32), ("balance_halves", i32),
@@ -194,6 +198,9 @@ SIGNATURES = {
     "cad_layer_ctx_set_comm": (C.c_int, [vp, vp]),
     "cad_layer_ctx_destroy": (C.c_int, [vp]),
     "cad_layer_begin": (C.c_int, [vp, vp]),
+    "cad_layer_begin_ex": (C.c_int, [vp, i32, vp]),
+    "cad_layer_step_ex": (C.c_int, [vp, P(cad_layer_io), i32, i32, vp]),
+    "cad_pp_tick_table": (C.c_int, [i64, i64, i32, P(cad_tick_work), i64, P(i64)]),
     "cad_dispatch": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp]),
     "cad_dispatch_ex": (C.c_int, [vp, i32, i32, i32, P(cad_layer_io), vp, vp]),
     "cad_layer_compute": (C.c_int, [vp, i32, i32, i32, vp]),

@@ -197,6 +197,7 @@ struct Peer {
   float* lse = nullptr;
   void* dq = nullptr;
   i64 home_rows = 0;
+  i64 q_pitch[2] = {1, 1};  // rows of the peer's server Q/LSE buffers per half
   Layout layout;
 };
 
@@ -380,26 +381,34 @@ struct cad_layer_ctx {
          "cad_copy_runs");
     }
   }
-  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) {
+  // [heads][rows] fp32 columns (LSE) of exchange x: dst_of(p) gives the
+  // peer's buffer and its row pitch
+  template <class DstOf>
+  void push_cols(int h, int x, const float* src, i64 src_rows, DstOf dst_of, cudaStream_t s, cudaStream_t local) {
     if (!move) return;
     for (int p = 0; p < W; ++p) {
-      const size_t a = run_off[h][kXO][static_cast<size_t>(p)], e = run_off[h][kXO][static_cast<size_t>(p) + 1];
+      const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
       if (a == e) continue;
-      const Peer& P = peer[static_cast<size_t>(p)];
+      const std::pair<float*, i64> dst = dst_of(p);
       if (p == me) {
-        const int64_t n = n_local_chunks[h][kXO];
+        const int64_t n = n_local_chunks[h][x];
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n, 148 * 4));
-        copy_col_chunks_kernel<<<grid, 256, 0, local>>>(d_local_chunks[h][kXO], n, src, src_rows, P.lse,
-                                                        P.home_rows, static_cast<int>(hq));
+        copy_col_chunks_kernel<<<grid, 256, 0, local>>>(d_local_chunks[h][x], n, src, src_rows, dst.first,
+                                                        dst.second, static_cast<int>(hq));
         cuda_check(cudaGetLastError(), "copy_col_chunks launch");
         ++launches;
         continue;
       }
       if (!move_remote) continue;
-      ok(cad_copy_runs_cols(runs[h][kXO].data() + a, static_cast<i64>(e - a), src, src_rows, P.lse, P.home_rows,
+      ok(cad_copy_runs_cols(runs[h][x].data() + a, static_cast<i64>(e - a), src, src_rows, dst.first, dst.second,
                             static_cast<int32_t>(hq), s),
          "cad_copy_runs_cols");
     }
+  }
+  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) {
+    push_cols(h, kXO, src, src_rows,
+              [&](int p) { return std::make_pair(peer[static_cast<size_t>(p)].lse, peer[static_cast<size_t>(p)].home_rows); },
+              s, local);
   }
 
   // NCCL: gather, all-to-allv, then scatter (or, with dst_contig, receive
@@ -414,13 +423,13 @@ struct cad_layer_ctx {
       launches += X.n_recv() > 0;
     }
   }
-  void nccl_lse(int h, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s) {
-    const XferRows& X = mine.half[h].x[kXO];
-    ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), d_send_idx[h][kXO], X.n_send(),
+  void nccl_cols(int h, int x, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s) {
+    const XferRows& X = mine.half[h].x[x];
+    ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), d_send_idx[h][x], X.n_send(),
                            static_cast<float*>(xsend), s),
        "cad_gather_cols_f32");
     alltoallv(X, lse_row, xrecv, s);
-    ok(cad_scatter_cols_f32(static_cast<const float*>(xrecv), d_recv_idx[h][kXO], X.n_recv(),
+    ok(cad_scatter_cols_f32(static_cast<const float*>(xrecv), d_recv_idx[h][x], X.n_recv(),
                             static_cast<int32_t>(hq), dst, dst_rows, s),
        "cad_scatter_cols_f32");
     launches += (X.n_send() > 0) + (X.n_recv() > 0);
@@ -455,8 +464,12 @@ struct cad_layer_ctx {
   }
 
   // ------------------------------------------------------------- phases
-  void begin(cudaStream_t s) {
+  int passes = CAD_PASS_BOTH;  // of the current step
+  void begin(cudaStream_t s, int passes_ = CAD_PASS_BOTH) {
     need_ready();
+    if (passes_ < CAD_PASS_FWD || passes_ > CAD_PASS_BOTH) throw cad::DomainError("passes must be FWD, BWD or BOTH");
+    if (passes_ != CAD_PASS_BOTH && NL != 1) throw cad::ConfigError("single-pass steps need layers == 1");
+    passes = passes_;
     g0 = gen;
     gen += 2 * static_cast<uint32_t>(NL);
     // every peer finished the previous step: its server buffers are free
@@ -479,6 +492,21 @@ struct cad_layer_ctx {
         nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s);
         nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s);
         nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s);
+      }
+    } else if (what == CAD_DISPATCH_FWD_STATE) {
+      // O and LSE rows home -> server, for a backward whose forward ran under
+      // another plan (a pipeline tick's backward, P/src/sim.cpp:326-353);
+      // ordered before the consumer by the DO dispatch's flag that follows
+      if (!io->o || !io->lse) throw cad::DomainError("null o/lse");
+      const i64 pitch = std::max<i64>(1, mine.half[h].q_rows);
+      if (flagged()) {
+        push(h, kXQ, io->o, q_row, [&](int p) { return peer_at(p, pb(p, l, h).o); }, s, local);
+        push_cols(h, kXQ, io->lse, mine.home_rows,
+                  [&](int p) { return std::make_pair(peer_at<float>(p, pb(p, l, h).lse), peer[static_cast<size_t>(p)].q_pitch[h]); },
+                  s, local);
+      } else if (move) {
+        nccl_rows(h, kXQ, io->o, q_row, at(B.o), false, s);
+        nccl_cols(h, kXQ, io->lse, mine.home_rows, at<float>(B.lse), pitch, s);
       }
     } else if (what == CAD_DISPATCH_DO) {
       if (!io->dout) throw cad::DomainError("null dout");
@@ -522,7 +550,7 @@ struct cad_layer_ctx {
         signal(F_O, h, gl(l), s);
       } else if (move) {
         nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s);
-        nccl_lse(h, at<float>(B.lse), qr, io->lse, mine.home_rows, s);
+        nccl_cols(h, kXO, at<float>(B.lse), qr, io->lse, mine.home_rows, s);
       }
     } else if (what == CAD_RETURN_GRAD) {
       if (flagged()) {
@@ -543,9 +571,13 @@ struct cad_layer_ctx {
   void finish(const cad_layer_io* io, cudaStream_t s) {
     if (flagged())
       for (int h = 0; h < 2; ++h) {
-        await(F_O, h, gl(NL - 1), s);
-        await(F_G, h, gb(0), s);
+        if (passes & CAD_PASS_FWD) await(F_O, h, gl(NL - 1), s);
+        if (passes & CAD_PASS_BWD) await(F_G, h, gb(0), s);
       }
+    if (!(passes & CAD_PASS_BWD)) {
+      if (flagged()) signal(F_DONE, 0, gdone(), s);
+      return;
+    }
     const i64 rows = mine.home_rows;
     const int chunks = static_cast<int>(hkv * d / 8);
     if (rows > 0 && (io->dk || io->dk_acc || io->dv || io->dv_acc)) {
@@ -566,7 +598,7 @@ struct cad_layer_ctx {
   // QKV arrived, dO arrived, forward done, backward done.
   int slot(int l, int h, int k) const { return 2 + ((l * 2 + h) * 4 + k); }
 
-  void step(const cad_layer_io* io, int mode, cudaStream_t comp) {
+  void step(const cad_layer_io* io, int mode, cudaStream_t comp, int passes_ = CAD_PASS_BOTH) {
     need_ready();
     // One thread enqueueing a whole step of rank 0 before rank 1's puts GPU
     // waits ahead of the work that releases them; streams of one context can
@@ -578,10 +610,12 @@ struct cad_layer_ctx {
       throw cad::ConfigError("cad_layer_step needs one process per rank (IPC or NCCL transport); drive LOCAL "
                              "contexts with the per-layer entry points in dependency order");
     if (mode == CAD_STEP_COMPUTE) {
-      for (int l = 0; l < NL; ++l)
-        for (int h = 0; h < 2; ++h) compute(l, h, false, comp, false, true);
-      for (int l = NL - 1; l >= 0; --l)
-        for (int h = 0; h < 2; ++h) compute(l, h, true, comp, false, true);
+      if (passes_ & CAD_PASS_FWD)
+        for (int l = 0; l < NL; ++l)
+          for (int h = 0; h < 2; ++h) compute(l, h, false, comp, false, true);
+      if (passes_ & CAD_PASS_BWD)
+        for (int l = NL - 1; l >= 0; --l)
+          for (int h = 0; h < 2; ++h) compute(l, h, true, comp, false, true);
       return;
     }
     if ((mode == CAD_STEP_SIGNAL || mode == CAD_STEP_COMM_LOCAL) && !flagged())
@@ -598,7 +632,7 @@ struct cad_layer_ctx {
     trace_reset(comp);
     cuda_check(cudaEventRecord(event(0), comp), "event");
     cuda_check(cudaStreamWaitEvent(comm, event(0), 0), "wait");
-    begin(comm);
+    begin(comm, passes_);
     auto disp = [&](int l, int h, int what) {
       const int m0 = tmark(comm);
       dispatch(l, h, what, io, comm, comp);
@@ -621,6 +655,22 @@ struct cad_layer_ctx {
       ret(l, h, what, io, comm, comp);
       trace_add(what == CAD_RETURN_O ? CAD_TRACE_RETURN_O : CAD_TRACE_RETURN_GRAD, l, h, m0, m0, tmark(comm));
     };
+    if (passes_ != CAD_PASS_BOTH) {  // one pass of one layer (a pipeline tick)
+      const bool bwd = passes_ == CAD_PASS_BWD;
+      for (int h = 0; h < 2; ++h) {
+        disp(0, h, CAD_DISPATCH_QKV);
+        if (bwd) {
+          disp(0, h, CAD_DISPATCH_FWD_STATE);
+          disp(0, h, CAD_DISPATCH_DO);
+        }
+        ca(0, h, bwd);
+      }
+      for (int h = 0; h < 2; ++h) back(0, h, bwd ? CAD_RETURN_GRAD : CAD_RETURN_O);
+      cuda_check(cudaEventRecord(event(1), comm), "event");
+      cuda_check(cudaStreamWaitEvent(comp, event(1), 0), "wait");
+      finish(io, comp);
+      return;
+    }
     // forward: comm D(0,0) D(1,0) dO(.,L-1) | R(0,l) D(0,l+1) | R(1,l) D(1,l+1) ...
     //          comp       F(0,0)    F(1,0)      F(0,l+1)         F(1,l+1)
     // so the return of half h and the next dispatch hide under CA(1-h)
@@ -754,6 +804,7 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     for (int p = 0; p < C->W; ++p) {
       Peer& P = C->peer[static_cast<size_t>(p)];
       P.home_rows = all[static_cast<size_t>(p)].home_rows;
+      for (int h = 0; h < 2; ++h) P.q_pitch[h] = std::max<i64>(1, all[static_cast<size_t>(p)].half[h].q_rows);
       P.layout = layout_of(all[static_cast<size_t>(p)], C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
     }
     // push runs: my send rows to p against p's receive rows from me
@@ -990,10 +1041,14 @@ int cad_layer_ctx_destroy(cad_layer_ctx* ctx) {
 }
 
 int cad_layer_begin(cad_layer_ctx* ctx, void* stream) {
+  return cad_layer_begin_ex(ctx, CAD_PASS_BOTH, stream);
+}
+
+int cad_layer_begin_ex(cad_layer_ctx* ctx, int32_t passes, void* stream) {
   return cad::guarded([&] {
     if (!ctx) throw cad::DomainError("null argument");
     cad_dev::DeviceGuard dg(ctx->device);
-    ctx->begin(static_cast<cudaStream_t>(stream));
+    ctx->begin(static_cast<cudaStream_t>(stream), passes);
   });
 }
 
@@ -1080,10 +1135,16 @@ int cad_layer_ctx_trace(cad_layer_ctx* ctx, cad_trace_rec* recs, int64_t cap, in
 }
 
 int cad_layer_step(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode, void* stream) {
+  return cad_layer_step_ex(ctx, io, mode, CAD_PASS_BOTH, stream);
+}
+
+int cad_layer_step_ex(cad_layer_ctx* ctx, const cad_layer_io* io, int32_t mode, int32_t passes, void* stream) {
   return cad::guarded([&] {
     if (!ctx) throw cad::DomainError("null argument");
+    if (passes < CAD_PASS_FWD || passes > CAD_PASS_BOTH) throw cad::DomainError("passes must be FWD, BWD or BOTH");
+    if (passes != CAD_PASS_BOTH && ctx->NL != 1) throw cad::ConfigError("single-pass steps need layers == 1");
     cad_dev::DeviceGuard dg(ctx->device);
-    ctx->step(io, mode, static_cast<cudaStream_t>(stream));
+    ctx->step(io, mode, static_cast<cudaStream_t>(stream), passes);
   });
 }
 

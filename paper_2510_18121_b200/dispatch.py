@@ -142,7 +142,8 @@ class Comm:
 
 TRANSPORTS = {"local": 0, "ipc": 1, "ce": 1, "nccl": 2}
 MODES = {"pingpong": 0, "serial": 1, "compute": 2, "comm": 3, "signal": 4, "comm_local": 5}
-DISPATCH_QKV, DISPATCH_DO = 0, 1
+DISPATCH_QKV, DISPATCH_DO, DISPATCH_FWD_STATE = 0, 1, 2
+PASSES = {"fwd": 1, "bwd": 2, "both": 3}
 RETURN_O, RETURN_GRAD = 0, 1
 
 
@@ -227,12 +228,14 @@ class DistCALayer:
         return N.cad_layer_io(_p(q), _p(k), _p(v), _p(do), _p(o), _p(lse), _p(dq), _p(dk), _p(dv),
                               _p(dk_acc), _p(dv_acc))
 
-    def step(self, io: N.cad_layer_io, mode: str = "pingpong", stream: Optional[torch.cuda.Stream] = None):
+    def step(self, io: N.cad_layer_io, mode: str = "pingpong", stream: Optional[torch.cuda.Stream] = None,
+             passes: str = "both"):
+        """One step; passes 'fwd' / 'bwd' run one pass (a pipeline tick)."""
         s = (stream or torch.cuda.current_stream(self.dev)).cuda_stream
-        check(lib().cad_layer_step(self._h, C.byref(io), MODES[mode], s))
+        check(lib().cad_layer_step_ex(self._h, C.byref(io), MODES[mode], PASSES[passes], s))
 
-    def begin(self, stream):
-        check(lib().cad_layer_begin(self._h, stream.cuda_stream))
+    def begin(self, stream, passes: str = "both"):
+        check(lib().cad_layer_begin_ex(self._h, PASSES[passes], stream.cuda_stream))
 
     def dispatch(self, layer, half, what, io, stream, local_stream=None):
         if local_stream is None:

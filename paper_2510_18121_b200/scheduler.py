@@ -369,3 +369,19 @@ def place_sequential(lengths: Sequence[int], num_devices: int, tokens_per_device
     out = (N.cad_item * max(1, n.value))()
     check(lib().cad_place_sequential(la, len(lengths), num_devices, tokens_per_device, out, n.value, C.byref(n)))
     return [Item.from_c(out[i]) for i in range(n.value)]
+
+
+PP_1F1B, PP_PHASE_SYNC = 0, 1
+
+
+def pp_tick_table(n_microbatches: int, n_stages: int, kind: int = PP_PHASE_SYNC):
+    """The pipeline tick table of simulate_pp_iteration (P/src/sim.cpp:297-353):
+    table[tick][stage] = None (idle) or (backward: bool, microbatch)."""
+    n = N.i64()
+    rc = lib().cad_pp_tick_table(n_microbatches, n_stages, kind, None, 0, C.byref(n))
+    if rc not in (N.CAD_OK, N.CAD_ERR_CAPACITY):
+        check(rc)
+    arr = (N.cad_tick_work * max(1, n.value * n_stages))()
+    check(lib().cad_pp_tick_table(n_microbatches, n_stages, kind, arr, n.value * n_stages, C.byref(n)))
+    return [[(bool(arr[t * n_stages + s].backward), arr[t * n_stages + s].microbatch)
+             if arr[t * n_stages + s].active else None for s in range(n_stages)] for t in range(n.value)]
