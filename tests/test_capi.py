@@ -74,3 +74,24 @@ def test_ca_plan_rejects_bad_shapes_without_gpu():
     assert N.lib().cad_ca_plan_create(tasks, 1, C.byref(shape), C.byref(h)) == N.CAD_ERR_CONFIG
     shape = N.cad_ca_shape(4, 2, 64, 0.0, 10, 10)
     assert N.lib().cad_ca_plan_create(tasks, 1, C.byref(shape), C.byref(h)) == N.CAD_ERR_CONFIG
+    # row offsets of the device task records are int32: buffers of >= 2^31 rows are refused
+    shape = N.cad_ca_shape(4, 2, 128, 0.0, 1 << 31, 10)
+    assert N.lib().cad_ca_plan_create(tasks, 1, C.byref(shape), C.byref(h)) == N.CAD_ERR_CONFIG
+    shape = N.cad_ca_shape(4, 2, 128, 0.0, 10, 1 << 31)
+    assert N.lib().cad_ca_plan_create(tasks, 1, C.byref(shape), C.byref(h)) == N.CAD_ERR_CONFIG
+
+
+def test_layer_ctx_rejects_bad_configs_without_gpu():
+    """cad_layer_cfg validation happens before any CUDA call."""
+    plan = S.PlanHandle([S.doc_item(0, 100, 0), S.doc_item(1, 100, 1)], 2, S.SchedulerConfig())
+    items = (N.cad_item * 2)(S.doc_item(0, 100, 0).to_c(), S.doc_item(1, 100, 1).to_c())
+    h = C.c_void_p()
+    for kw, code in ((dict(rank=2), N.CAD_ERR_DOMAIN), (dict(world=3), N.CAD_ERR_CONFIG),
+                     (dict(head_dim=64), N.CAD_ERR_CONFIG), (dict(h_kv=3), N.CAD_ERR_CONFIG),
+                     (dict(transport=7), N.CAD_ERR_CONFIG), (dict(layers=0), N.CAD_ERR_CONFIG)):
+        args = dict(rank=0, world=2, h_q=8, h_kv=2, head_dim=128, softmax_scale=0.0, transport=1, layers=1)
+        args.update(kw)
+        cfg = N.cad_layer_cfg(args["rank"], args["world"], args["h_q"], args["h_kv"], args["head_dim"],
+                              args["softmax_scale"], args["transport"], args["layers"], 0, 0)
+        assert N.lib().cad_layer_ctx_create(plan.h, items, 2, C.byref(cfg), C.byref(h)) == code, kw
+    plan.close()
