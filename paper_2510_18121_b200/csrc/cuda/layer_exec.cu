@@ -324,7 +324,6 @@ struct cad_layer_ctx {
   std::vector<cudaEvent_t> ev;
   uint32_t gen = 0, g0 = 0;
   i64 launches = 0;
-  bool move = true;         // false: no row copies at all (NCCL: no exchange)
   bool move_remote = true;  // false: signal mode -- this rank's own rows still
                             // move, the transfers to peers shrink to their flags
 
@@ -361,7 +360,6 @@ struct cad_layer_ctx {
   // pushes queued behind it)
   template <class DstOf>
   void push(int h, int x, const void* src, i64 row_bytes, DstOf dst_of, cudaStream_t s, cudaStream_t local) {
-    if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
       if (a == e) continue;
@@ -385,7 +383,6 @@ struct cad_layer_ctx {
   // peer's buffer and its row pitch
   template <class DstOf>
   void push_cols(int h, int x, const float* src, i64 src_rows, DstOf dst_of, cudaStream_t s, cudaStream_t local) {
-    if (!move) return;
     for (int p = 0; p < W; ++p) {
       const size_t a = run_off[h][x][static_cast<size_t>(p)], e = run_off[h][x][static_cast<size_t>(p) + 1];
       if (a == e) continue;
@@ -488,7 +485,7 @@ struct cad_layer_ctx {
         push(h, kXKV, io->k, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).k); }, s, local);
         push(h, kXKV, io->v, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).v); }, s, local);
         signal(F_QKV, h, gl(l), s);
-      } else if (move) {
+      } else {
         nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s);
         nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s);
         nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s);
@@ -504,7 +501,7 @@ struct cad_layer_ctx {
         push_cols(h, kXQ, io->lse, mine.home_rows,
                   [&](int p) { return std::make_pair(peer_at<float>(p, pb(p, l, h).lse), peer[static_cast<size_t>(p)].q_pitch[h]); },
                   s, local);
-      } else if (move) {
+      } else {
         nccl_rows(h, kXQ, io->o, q_row, at(B.o), false, s);
         nccl_cols(h, kXQ, io->lse, mine.home_rows, at<float>(B.lse), pitch, s);
       }
@@ -514,7 +511,7 @@ struct cad_layer_ctx {
         if (l < NL - 1) await(F_G, h, gb(l + 1), s);  // dQ(h, l+1) home -> dO(h, l)
         push(h, kXQ, io->dout, q_row, [&](int p) { return peer_at(p, pb(p, l, h).dout); }, s, local);
         signal(F_DO, h, gb(l), s);
-      } else if (move) {
+      } else {
         nccl_rows(h, kXQ, io->dout, q_row, at(B.dout), false, s);
       }
     } else {
@@ -548,7 +545,7 @@ struct cad_layer_ctx {
         push(h, kXO, at(B.o), q_row, [&](int p) { return peer[static_cast<size_t>(p)].o; }, s, local);
         push_lse(h, at<float>(B.lse), qr, s, local);
         signal(F_O, h, gl(l), s);
-      } else if (move) {
+      } else {
         nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s);
         nccl_cols(h, kXO, at<float>(B.lse), qr, io->lse, mine.home_rows, s);
       }
@@ -558,7 +555,7 @@ struct cad_layer_ctx {
         push(h, kXKR, at(B.dk), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdk); }, s, local);
         push(h, kXKR, at(B.dv), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdv); }, s, local);
         signal(F_G, h, gb(l), s);
-      } else if (move) {
+      } else {
         nccl_rows(h, kXO, at(B.dq), q_row, io->dq, false, s);
         nccl_rows(h, kXKR, at(B.dk), kv_row, at(B.sdk), true, s);  // partials land in recv order
         nccl_rows(h, kXKR, at(B.dv), kv_row, at(B.sdv), true, s);
@@ -582,7 +579,7 @@ struct cad_layer_ctx {
     const int chunks = static_cast<int>(hkv * d / 8);
     if (rows > 0 && (io->dk || io->dk_acc || io->dv || io->dv_acc)) {
       const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
-      const int n_layers = move ? NL : 0;
+      const int n_layers = NL;
       reduce_partials_kernel<<<blocks, 256, 0, s>>>(d_red_off, d_red_ent, d_red_src[0], n_layers, rows, chunks,
                                                     static_cast<uint4*>(io->dk), reinterpret_cast<float4*>(io->dk_acc));
       reduce_partials_kernel<<<blocks, 256, 0, s>>>(d_red_off, d_red_ent, d_red_src[1], n_layers, rows, chunks,
