@@ -67,6 +67,17 @@ def main():
         torch.cuda.synchronize()
         results[mode] = {n: t.float().cpu().numpy() for n, t in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk),
                                                                   ("dv", dv))}
+    if layers == 1:
+        # a forward-only step, then a backward-only step that re-dispatches Q/K/V
+        # and the forward state (O, LSE) with dO: the two passes of a pipeline tick
+        o.fill_(float("nan")); dq.fill_(float("nan")); lse.fill_(float("nan"))
+        layer.step(io, "pingpong", passes="fwd")
+        torch.cuda.synchronize()
+        fwd_o, fwd_lse = o.float().cpu().numpy(), lse.cpu().numpy()
+        layer.step(io, "pingpong", passes="bwd")
+        torch.cuda.synchronize()
+        results["split-passes"] = {"o": fwd_o, "lse": fwd_lse, "dq": dq.float().cpu().numpy(),
+                                   "dk": dk.float().cpu().numpy(), "dv": dv.float().cpu().numpy()}
     # the CPU oracle on the whole batch (every document one task), in this rank's home rows
     tasks, off = [], 0
     for l in lengths:
