@@ -826,6 +826,16 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       cuda_check(cudaGetLastError(), "ca_delta launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
     }
+    // 2-3. dK/dV on `stream`, dQ forked onto the plan's side stream (joined
+    // back below) when both run: CAD_BWD_FORK=0 keeps them in order on `stream`
+    static const bool fork_off = std::getenv("CAD_BWD_FORK") && std::getenv("CAD_BWD_FORK")[0] == '0';
+    const bool fork = !fork_off && (parts & CAD_BWD_DKDV) && (parts & CAD_BWD_DQ) && plan->side;
+    cudaStream_t s_dq = s;
+    if (fork) {
+      cuda_check(cudaEventRecord(plan->ev_fork, s), "event(fork)");
+      cuda_check(cudaStreamWaitEvent(plan->side, plan->ev_fork, 0), "wait(fork)");
+      s_dq = plan->side;
+    }
     // 2. dK, dV (CTA pairs unless CAD_DKDV_PAIR=0)
     static const bool dkdv_pair_off = std::getenv("CAD_DKDV_PAIR") && std::getenv("CAD_DKDV_PAIR")[0] == '0';
     if ((parts & CAD_BWD_DKDV) && !dkdv_pair_off &&
@@ -859,8 +869,8 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
     // 3. dQ (CTA pairs for even GQA groups unless CAD_DQ_PAIR=0)
     static const bool dq_pair_off = std::getenv("CAD_DQ_PAIR") && std::getenv("CAD_DQ_PAIR")[0] == '0';
     if ((parts & CAD_BWD_DQ) && !dq_pair_off &&
-        launch_dq_pair(plan, q, k, v, dout, lse2, delta, pitch, dq, s)) {
-      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq_pair");
+        launch_dq_pair(plan, q, k, v, dout, lse2, delta, pitch, dq, s_dq)) {
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s_dq), "ca_bwd_dq_pair");
     } else if (parts & CAD_BWD_DQ) {
       dq::Params p;
       make_tile_map(&p.tm_q, q, sh.q_rows, sh.h_q);
@@ -880,9 +890,13 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       p.scale = sh.softmax_scale;
       p.scale_log2 = sh.softmax_scale * kLog2e;
       const int grid = plan->sched_dq.G;
-      dq::ca_bwd_dq_kernel<<<grid, kThreads, dq::kSmemBytes, s>>>(p);
+      dq::ca_bwd_dq_kernel<<<grid, kThreads, dq::kSmemBytes, s_dq>>>(p);
       cuda_check(cudaGetLastError(), "ca_bwd_dq launch");
-      if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dq");
+      if (debug_sync) cuda_check(cudaStreamSynchronize(s_dq), "ca_bwd_dq");
+    }
+    if (fork) {
+      cuda_check(cudaEventRecord(plan->ev_join, plan->side), "event(join)");
+      cuda_check(cudaStreamWaitEvent(s, plan->ev_join, 0), "wait(join)");
     }
   });
 }

@@ -94,6 +94,11 @@ struct cad_ca_plan {
   }
   // LPT work lists per kernel for the current grid (rebuilt by set_max_ctas)
   cad_dev::CtaLists sched_fwd, sched_fwd2, sched_dq, sched_dq2, sched_kv, sched_kv2;
+  // backward fork/join: dQ runs on a side stream next to dK/dV, so dQ's CTAs
+  // take the SMs dK/dV's retire from (its LPT tail) instead of waiting for the
+  // last dK/dV CTA
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace cad_dev {

@@ -352,6 +352,9 @@ int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks, const cad_ca_s
     upload(P->kv2_units, &P->d_kv2);
     upload(P->kv_segs, &P->d_segs);
     cad_dev::build_schedules(*P);
+    cuda_check(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+    cuda_check(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming), "cudaEventCreate");
     *plan = P.release();
   });
 }
@@ -396,6 +399,9 @@ int cad_ca_plan_destroy(cad_ca_plan* plan) {
     for (cad_dev::CtaLists* L : {&plan->sched_fwd, &plan->sched_fwd2, &plan->sched_dq, &plan->sched_dq2,
                                  &plan->sched_kv, &plan->sched_kv2})
       cudaFree(L->d);
+    if (plan->side) cudaStreamDestroy(plan->side);
+    if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+    if (plan->ev_join) cudaEventDestroy(plan->ev_join);
     delete plan;
   });
 }
