@@ -826,10 +826,11 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       cuda_check(cudaGetLastError(), "ca_delta launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
     }
-    // 2-3. dK/dV on `stream`, dQ forked onto the plan's side stream (joined
-    // back below) when both run: CAD_BWD_FORK=0 keeps them in order on `stream`
-    static const bool fork_off = std::getenv("CAD_BWD_FORK") && std::getenv("CAD_BWD_FORK")[0] == '0';
-    const bool fork = !fork_off && (parts & CAD_BWD_DKDV) && (parts & CAD_BWD_DQ) && plan->side;
+    // 2-3. dK/dV then dQ on `stream`; CAD_BWD_FORK=1 forks dQ onto the plan's
+    // side stream (joined back below) so its CTAs take the SMs dK/dV's tail
+    // frees -- measured 0.5-1 % slower, hence off by default
+    static const bool fork_on = std::getenv("CAD_BWD_FORK") && std::getenv("CAD_BWD_FORK")[0] == '1';
+    const bool fork = fork_on && (parts & CAD_BWD_DKDV) && (parts & CAD_BWD_DQ) && plan->side;
     cudaStream_t s_dq = s;
     if (fork) {
       cuda_check(cudaEventRecord(plan->ev_fork, s), "event(fork)");

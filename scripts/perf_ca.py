@@ -44,7 +44,8 @@ for name, (fn, fl) in runs.items():
     ms = st.elapsed_time(en) / reps
     tot += ms
     print(f"{name:6s} {ms:8.2f} ms  {fl / ms / 1e9 if fl else 0:8.1f} TFLOP/s (executed)")
-print(f"total  {tot:8.2f} ms  {3.5 * F / tot / 1e9:8.1f} TFLOP/s (algorithmic fwd+bwd, parts)")
+if tot > 0:
+    print(f"total  {tot:8.2f} ms  {3.5 * F / tot / 1e9:8.1f} TFLOP/s (algorithmic fwd+bwd, parts)")
 if only and "bwd" not in only:
     sys.exit(0)
 fn, fl = runs["bwd"]
