@@ -307,8 +307,16 @@ struct cad_layer_ctx {
   std::vector<size_t> run_off[2][4];  // per peer: first run (W + 1 entries)
   int64_t* d_local_chunks[2][4] = {};  // this rank's own rows: device chunk lists
   int64_t n_local_chunks[2][4] = {};
-  i64* d_send_idx[2][4] = {};
-  i64* d_recv_idx[2][4] = {};
+  // NCCL: row lists without this rank's own rows (those move by the local
+  // copy kernels), counts with the self entry zeroed, and the original
+  // receive offsets (partials land in the staging at their full-order rows)
+  struct NcclX {
+    std::vector<i64> sc, rc, rd_full;
+    i64 n_send = 0, n_recv = 0;
+    i64* d_send = nullptr;
+    i64* d_recv = nullptr;
+  };
+  NcclX nx[2][4];
   int64_t* d_red_off = nullptr;  // dK/dV reduction CSR over home rows
   int32_t* d_red_ent = nullptr;  // (row << 2) | (own << 1) | half
   const uint4** d_red_src[2] = {nullptr, nullptr};  // dK, dV bases [layer][own][half]
@@ -410,39 +418,57 @@ struct cad_layer_ctx {
 
   // NCCL: gather, all-to-allv, then scatter (or, with dst_contig, receive
   // straight into a buffer in recv order)
-  void nccl_rows(int h, int x, const void* src, i64 row_bytes, void* dst, bool dst_contig, cudaStream_t s) {
-    const XferRows& X = mine.half[h].x[x];
-    ok(cad_gather_rows(src, d_send_idx[h][x], X.n_send(), row_bytes, xsend, s), "cad_gather_rows");
-    launches += X.n_send() > 0;
-    alltoallv(X, row_bytes, dst_contig ? dst : xrecv, s);
+  void nccl_rows(int h, int x, const void* src, i64 row_bytes, void* dst, bool dst_contig, cudaStream_t s,
+                 cudaStream_t local) {
+    const NcclX& X = nx[h][x];
+    ok(cad_gather_rows(src, X.d_send, X.n_send, row_bytes, xsend, s), "cad_gather_rows");
+    launches += X.n_send > 0;
+    alltoallv(X, row_bytes, dst_contig ? dst : xrecv, dst_contig, s);
     if (!dst_contig) {
-      ok(cad_scatter_rows(xrecv, d_recv_idx[h][x], X.n_recv(), row_bytes, dst, s), "cad_scatter_rows");
-      launches += X.n_recv() > 0;
+      ok(cad_scatter_rows(xrecv, X.d_recv, X.n_recv, row_bytes, dst, s), "cad_scatter_rows");
+      launches += X.n_recv > 0;
+    }
+    // own rows: one local copy kernel (own dK/dV partials are read in place)
+    if (x != kXKR && n_local_chunks[h][x] > 0) {
+      const int64_t n = n_local_chunks[h][x];
+      copy_row_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(n, 148 * 4)), 256, 0, local>>>(
+          d_local_chunks[h][x], n, static_cast<const uint4*>(src), static_cast<uint4*>(dst), row_bytes / 16);
+      cuda_check(cudaGetLastError(), "copy_row_chunks launch");
+      ++launches;
     }
   }
-  void nccl_cols(int h, int x, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s) {
-    const XferRows& X = mine.half[h].x[x];
-    ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), d_send_idx[h][x], X.n_send(),
+  void nccl_cols(int h, int x, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s,
+                 cudaStream_t local) {
+    const NcclX& X = nx[h][x];
+    ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), X.d_send, X.n_send,
                            static_cast<float*>(xsend), s),
        "cad_gather_cols_f32");
-    alltoallv(X, lse_row, xrecv, s);
-    ok(cad_scatter_cols_f32(static_cast<const float*>(xrecv), d_recv_idx[h][x], X.n_recv(),
-                            static_cast<int32_t>(hq), dst, dst_rows, s),
+    alltoallv(X, lse_row, xrecv, false, s);
+    ok(cad_scatter_cols_f32(static_cast<const float*>(xrecv), X.d_recv, X.n_recv, static_cast<int32_t>(hq), dst,
+                            dst_rows, s),
        "cad_scatter_cols_f32");
-    launches += (X.n_send() > 0) + (X.n_recv() > 0);
+    launches += (X.n_send > 0) + (X.n_recv > 0);
+    if (n_local_chunks[h][x] > 0) {
+      const int64_t n = n_local_chunks[h][x];
+      copy_col_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(n, 148 * 4)), 256, 0, local>>>(
+          d_local_chunks[h][x], n, src, src_rows, dst, dst_rows, static_cast<int>(hq));
+      cuda_check(cudaGetLastError(), "copy_col_chunks launch");
+      ++launches;
+    }
   }
-  void alltoallv(const XferRows& X, i64 row_bytes, void* recv, cudaStream_t s) const {
+  void alltoallv(const NcclX& X, i64 row_bytes, void* recv, bool full_order, cudaStream_t s) const {
     if (!comm) throw cad::ConfigError("NCCL transport: cad_layer_ctx_set_comm was not called");
     std::vector<i64> sb(static_cast<size_t>(W)), sd(static_cast<size_t>(W)), rb(static_cast<size_t>(W)),
         rd(static_cast<size_t>(W));
     i64 so = 0, ro = 0;
     for (int p = 0; p < W; ++p) {
-      sb[static_cast<size_t>(p)] = X.send_counts[static_cast<size_t>(p)] * row_bytes;
-      rb[static_cast<size_t>(p)] = X.recv_counts[static_cast<size_t>(p)] * row_bytes;
-      sd[static_cast<size_t>(p)] = so;
-      rd[static_cast<size_t>(p)] = ro;
-      so += sb[static_cast<size_t>(p)];
-      ro += rb[static_cast<size_t>(p)];
+      const size_t q = static_cast<size_t>(p);
+      sb[q] = X.sc[q] * row_bytes;
+      rb[q] = X.rc[q] * row_bytes;
+      sd[q] = so;
+      rd[q] = full_order ? X.rd_full[q] * row_bytes : ro;
+      so += sb[q];
+      ro += rb[q];
     }
     ok(cad_alltoallv(comm, xsend, sb.data(), sd.data(), recv, rb.data(), rd.data(), s), "cad_alltoallv");
   }
@@ -486,9 +512,9 @@ struct cad_layer_ctx {
         push(h, kXKV, io->v, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).v); }, s, local);
         signal(F_QKV, h, gl(l), s);
       } else {
-        nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s);
-        nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s);
-        nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s);
+        nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s, local);
+        nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s, local);
+        nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s, local);
       }
     } else if (what == CAD_DISPATCH_FWD_STATE) {
       // O and LSE rows home -> server, for a backward whose forward ran under
@@ -502,8 +528,8 @@ struct cad_layer_ctx {
                   [&](int p) { return std::make_pair(peer_at<float>(p, pb(p, l, h).lse), peer[static_cast<size_t>(p)].q_pitch[h]); },
                   s, local);
       } else {
-        nccl_rows(h, kXQ, io->o, q_row, at(B.o), false, s);
-        nccl_cols(h, kXQ, io->lse, mine.home_rows, at<float>(B.lse), pitch, s);
+        nccl_rows(h, kXQ, io->o, q_row, at(B.o), false, s, local);
+        nccl_cols(h, kXQ, io->lse, mine.home_rows, at<float>(B.lse), pitch, s, local);
       }
     } else if (what == CAD_DISPATCH_DO) {
       if (!io->dout) throw cad::DomainError("null dout");
@@ -512,7 +538,7 @@ struct cad_layer_ctx {
         push(h, kXQ, io->dout, q_row, [&](int p) { return peer_at(p, pb(p, l, h).dout); }, s, local);
         signal(F_DO, h, gb(l), s);
       } else {
-        nccl_rows(h, kXQ, io->dout, q_row, at(B.dout), false, s);
+        nccl_rows(h, kXQ, io->dout, q_row, at(B.dout), false, s, local);
       }
     } else {
       throw cad::DomainError("unknown dispatch kind");
@@ -546,8 +572,8 @@ struct cad_layer_ctx {
         push_lse(h, at<float>(B.lse), qr, s, local);
         signal(F_O, h, gl(l), s);
       } else {
-        nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s);
-        nccl_cols(h, kXO, at<float>(B.lse), qr, io->lse, mine.home_rows, s);
+        nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s, local);
+        nccl_cols(h, kXO, at<float>(B.lse), qr, io->lse, mine.home_rows, s, local);
       }
     } else if (what == CAD_RETURN_GRAD) {
       if (flagged()) {
@@ -556,9 +582,9 @@ struct cad_layer_ctx {
         push(h, kXKR, at(B.dv), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdv); }, s, local);
         signal(F_G, h, gb(l), s);
       } else {
-        nccl_rows(h, kXO, at(B.dq), q_row, io->dq, false, s);
-        nccl_rows(h, kXKR, at(B.dk), kv_row, at(B.sdk), true, s);  // partials land in recv order
-        nccl_rows(h, kXKR, at(B.dv), kv_row, at(B.sdv), true, s);
+        nccl_rows(h, kXO, at(B.dq), q_row, io->dq, false, s, local);
+        nccl_rows(h, kXKR, at(B.dk), kv_row, at(B.sdk), true, s, local);  // partials land in recv order
+        nccl_rows(h, kXKR, at(B.dv), kv_row, at(B.sdv), true, s, local);
       }
     } else {
       throw cad::DomainError("unknown return kind");
@@ -740,8 +766,8 @@ struct cad_layer_ctx {
       if (plan[h]) cad_ca_plan_destroy(plan[h]);
       cudaFree(ws[h]);
       for (int x = 0; x < 4; ++x) {
-        cudaFree(d_send_idx[h][x]);
-        cudaFree(d_recv_idx[h][x]);
+        cudaFree(nx[h][x].d_send);
+        cudaFree(nx[h][x].d_recv);
         cudaFree(d_local_chunks[h][x]);
       }
       cudaFree(d_red_src[h]);
@@ -854,8 +880,29 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
       const HalfRows& H = C->mine.half[h];
       for (const cad_ca_task& t : H.tasks) C->pairs += cad_causal_pairs(t.n_q, t.kv_len);
       for (int x = 0; x < 4; ++x) {
-        C->d_send_idx[h][x] = dev_copy(H.x[x].send_idx);
-        C->d_recv_idx[h][x] = dev_copy(H.x[x].recv_idx);
+        if (cfg->transport == CAD_TRANSPORT_NCCL) {
+          const XferRows& X = H.x[x];
+          cad_layer_ctx::NcclX& N = C->nx[h][x];
+          std::vector<i64> si, ri;
+          i64 so = 0, ro = 0;
+          for (int p = 0; p < C->W; ++p) {
+            const size_t q = static_cast<size_t>(p);
+            const i64 ns = X.send_counts[q], nr = X.recv_counts[q];
+            N.rd_full.push_back(ro);
+            if (p != C->me) {
+              si.insert(si.end(), X.send_idx.begin() + so, X.send_idx.begin() + so + ns);
+              ri.insert(ri.end(), X.recv_idx.begin() + ro, X.recv_idx.begin() + ro + nr);
+            }
+            N.sc.push_back(p == C->me ? 0 : ns);
+            N.rc.push_back(p == C->me ? 0 : nr);
+            so += ns;
+            ro += nr;
+          }
+          N.n_send = static_cast<i64>(si.size());
+          N.n_recv = static_cast<i64>(ri.size());
+          N.d_send = dev_copy(si);
+          N.d_recv = dev_copy(ri);
+        }
         xmax = std::max(xmax, static_cast<size_t>(std::max(H.x[x].n_send(), H.x[x].n_recv()) * C->q_row));
       }
       if (H.tasks.empty()) continue;
