@@ -268,6 +268,9 @@ def run(args, metric, load_peaks, ClockSampler):
             "comm": {"ms_compute_only": ms_compute, "ms_signal": ms_signal, "ms_comm_only": ms_comm,
                      "ms_comm_local_only": ms_comm_local, "ms_wire": wire_ms,
                      "ms_serial": ms_serial, "ms_pingpong": ms, "hidden_fraction": hidden,
+                     # the peer transfers' cost as the step sees it: ping-pong minus the same
+                     # step with every peer transfer shrunk to its flag
+                     "exposed_wire_ms": ms - ms_signal, "exposed_wire_share_of_step": (ms - ms_signal) / ms,
                      "hidden_fraction_all_movement": hidden_vs_compute,
                      "nccl": nccl,
                      "wire_bytes_per_step_max_rank": float(allst[:, 2].max()),
