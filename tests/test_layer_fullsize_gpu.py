@@ -1,0 +1,89 @@
+"""BASELINE config 3 proper on ONE GPU: 524 288 tokens (pretrain_upsampled seed
+1, Llama-3-8B shape 32 Q / 8 KV heads) scheduled bit-exactly over 8 ranks and
+executed as one layer through the per-layer executor with all 8 ranks'
+contexts in this process (CAD_TRANSPORT_LOCAL, phase by phase): every home
+row's O, LSE, dQ, dK, dV is compared with the same batch computed whole by
+the single-server kernels (whose full-size correctness against a float64
+restatement is tests/test_ca_full_size_gpu.py). Also config 5's uniform[1,4K]
+mix (~280 documents) over 8 ranks."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind", ["pretrain", "uniform"])
+def test_config3_scale_layer_over_8_ranks_on_one_gpu(kind):
+    from paper_2510_18121_b200 import configs as CF
+    from paper_2510_18121_b200 import dispatch as D
+    from paper_2510_18121_b200 import scheduler as S
+    from paper_2510_18121_b200.ca import CAPlan, CATaskRows
+    dev = torch.device("cuda", 0)
+    world, per = 8, 65536
+    shape = CF.LLAMA8B
+    hq, hkv = shape.h_q, shape.h_kv
+    lengths = S.sample_batch(CF.length_dist(kind, 1), world * per)
+    T = sum(lengths)
+    g = torch.Generator(device=dev).manual_seed(17)
+    bf = dict(device=dev, dtype=torch.bfloat16)
+    q = torch.randn(T, hq, 128, generator=g, **bf)
+    k = torch.randn(T, hkv, 128, generator=g, **bf)
+    v = torch.randn(T, hkv, 128, generator=g, **bf)
+    do = torch.randn(T, hq, 128, generator=g, **bf)
+    # the whole batch on one server
+    tasks, off = [], 0
+    for L in lengths:
+        tasks.append(CATaskRows(off, L, off, L))
+        off += L
+    ref = CAPlan(tasks, hq, hkv, T, T)
+    ro, rlse = ref.forward(q, k, v)
+    rdq, rdk, rdv = ref.backward(q, k, v, ro, rlse, do)
+    ref.close()
+    # 8 ranks: place_sequential homes are consecutive 65 536-row slices
+    plans = [D.LayerPlan(lengths, world, r, shape) for r in range(world)]
+    moved = sum(1 for t in plans[0].plan.tasks if t.assigned_server != t.source_device)
+    layers = [D.DistCALayer(plans[r], dev, "local") for r in range(world)]
+    out = {n: torch.full_like(t, float("nan")) for n, t in (("o", q), ("dq", q), ("dk", k), ("dv", v))}
+    lse = torch.full((hq, T), float("nan"), device=dev)
+    lse_r = [torch.empty(hq, per, device=dev) for _ in range(world)]
+    ios = []
+    for r, L in enumerate(layers):
+        assert L.home_rows == per
+        sl = slice(r * per, (r + 1) * per)
+        L.bind_outputs(out["o"][sl], lse_r[r], out["dq"][sl])
+        ios.append(L.io(q[sl], k[sl], v[sl], do[sl], out["o"][sl], lse_r[r], out["dq"][sl], out["dk"][sl],
+                        out["dv"][sl]))
+    blobs = [L.export() for L in layers]
+    for L in layers:
+        L.connect(blobs)
+    st = torch.cuda.current_stream(dev)
+    for L in layers:
+        L.begin(st)
+    for what, bwd, ret in ((D.DISPATCH_QKV, False, D.RETURN_O), (D.DISPATCH_DO, True, D.RETURN_GRAD)):
+        for h in (0, 1):
+            for r, L in enumerate(layers):
+                L.dispatch(0, h, what, ios[r], st)
+        for h in (0, 1):
+            for L in layers:
+                L.compute(0, h, bwd, st)
+        for h in (0, 1):
+            for r, L in enumerate(layers):
+                L.ret(0, h, ret, ios[r], st)
+    for r, L in enumerate(layers):
+        L.finish(ios[r], st)
+    torch.cuda.synchronize()
+    for r in range(world):
+        lse[:, r * per:(r + 1) * per] = lse_r[r]
+    for L in layers:
+        L.close()
+    print(f"{kind}: {len(lengths)} docs, {len(plans[0].plan.tasks)} tasks, {moved} served remotely")
+    for name, got, want in (("o", out["o"], ro), ("dq", out["dq"], rdq), ("dk", out["dk"], rdk),
+                            ("dv", out["dv"], rdv)):
+        assert torch.isfinite(got).all(), name
+        err = (got.float() - want.float()).abs().amax(dim=(1, 2))
+        mag = want.float().abs().amax(dim=(1, 2)).clamp(min=1.0)
+        print(f"  {name}: max abs {err.max().item():.3e}, worst row rel {(err / mag).max().item():.3e}")
+        assert (err / mag).max().item() <= 1e-2, name
+    lerr = (lse - rlse).abs().max().item()
+    print(f"  lse: max abs {lerr:.3e}")
+    assert lerr <= 1e-4
