@@ -383,9 +383,50 @@ struct cad_layer_ctx {
         continue;
       }
       if (!move_remote) continue;
-      ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes, s),
-         "cad_copy_runs");
+      if (lanes.empty()) {
+        ok(cad_copy_runs(runs[h][x].data() + a, static_cast<i64>(e - a), src, dst_of(p), row_bytes, s),
+           "cad_copy_runs");
+        continue;
+      }
+      for (size_t i = a; i < e; ++i) {  // split into <= kLanePiece pieces over the lanes
+        const cad_run& r = runs[h][x][i];
+        const char* sp = static_cast<const char*>(src) + r.src_row * row_bytes;
+        char* dp = static_cast<char*>(dst_of(p)) + r.dst_row * row_bytes;
+        for (i64 off = 0, n = r.n_rows * row_bytes; off < n; off += kLanePiece)
+          pieces.push_back({sp + off, dp + off, std::min<i64>(kLanePiece, n - off)});
+      }
     }
+    flush_pieces(s);
+  }
+
+  // CAD_PUSH_LANES=k (k > 1): remote pushes spread over k extra streams (forked
+  // from and joined back into the pushing stream), so several copy engines
+  // drive NVLink at once
+  static constexpr i64 kLanePiece = 16 << 20;
+  std::vector<cudaStream_t> lanes;
+  std::vector<cudaEvent_t> lane_ev;  // [0] fork, [1..k] joins
+  struct Piece {
+    const char* src;
+    char* dst;
+    i64 bytes;
+  };
+  std::vector<Piece> pieces;
+  void flush_pieces(cudaStream_t s) {
+    if (pieces.empty()) return;
+    cuda_check(cudaEventRecord(lane_ev[0], s), "event(fork)");
+    std::vector<i64> load(lanes.size(), 0);
+    for (size_t k = 0; k < lanes.size(); ++k) cuda_check(cudaStreamWaitEvent(lanes[k], lane_ev[0], 0), "wait");
+    for (const Piece& pc : pieces) {
+      const size_t k = static_cast<size_t>(std::min_element(load.begin(), load.end()) - load.begin());
+      cuda_check(cudaMemcpyAsync(pc.dst, pc.src, static_cast<size_t>(pc.bytes), cudaMemcpyDeviceToDevice, lanes[k]),
+                 "cudaMemcpyAsync(lane)");
+      load[k] += pc.bytes;
+    }
+    for (size_t k = 0; k < lanes.size(); ++k) {
+      cuda_check(cudaEventRecord(lane_ev[k + 1], lanes[k]), "event(join)");
+      cuda_check(cudaStreamWaitEvent(s, lane_ev[k + 1], 0), "wait(join)");
+    }
+    pieces.clear();
   }
   // [heads][rows] fp32 columns (LSE) of exchange x: dst_of(p) gives the
   // peer's buffer and its row pitch
@@ -779,6 +820,8 @@ struct cad_layer_ctx {
     cudaFree(xrecv);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    for (cudaEvent_t e : lane_ev) cudaEventDestroy(e);
+    for (cudaStream_t st : lanes) cudaStreamDestroy(st);
     if (comm_stream) cudaStreamDestroy(comm_stream);
   }
 };
@@ -969,6 +1012,17 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
       cuda_check(cudaMalloc(&C->xrecv, xmax), "cudaMalloc(recv)");
     }
     cuda_check(cudaStreamCreateWithFlags(&C->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (const char* e = std::getenv("CAD_PUSH_LANES")) {
+      const int k = std::atoi(e);
+      for (int i = 0; k > 1 && i < k; ++i) {
+        cudaStream_t st;
+        cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(lane)");
+        C->lanes.push_back(st);
+      }
+      C->lane_ev.resize(C->lanes.empty() ? 0 : C->lanes.size() + 1);
+      for (cudaEvent_t& ev : C->lane_ev)
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate(lane)");
+    }
     C->ev.resize(static_cast<size_t>(2 + 8 * C->NL));
     for (cudaEvent_t& e : C->ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
