@@ -201,7 +201,7 @@ def reference_arm(args, rank):
         "impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": CFG2_WORKLOAD, "sample": sample,
+        "config": {"workload": wl_name, "workload_id": workload, "sample": sample,
                    "extrapolated_config2_step_s": cfg2_flops / (tf * 1e12) if tf > 0 else None},
         "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": nth, "cpu_model": cpu_model(),
                          "kind": "port", "sample": sample, "scheduler_ref": sched},
@@ -232,8 +232,29 @@ def single_gpu(args):
     from paper_2510_18121_b200 import scheduler as S
     from paper_2510_18121_b200.ca import BWD_DELTA, BWD_DKDV, BWD_DQ, CAPlan, CATaskRows
 
-    shape = CF.LLAMA8B
-    lengths = S.sample_batch(CF.length_dist("pretrain", SEED), 131072)
+    # CAD_WORKLOAD (builder runs; the default is BASELINE config 2): cfg3 = one
+    # GPU's 65 536 tokens of config 3 (the weak-scaling base), cfg4 =
+    # config 4's 1M-token 34B batch on one GPU (the strong-scaling base of the
+    # N>1 lines), cfg5-<dist> = one GPU's 65 536 tokens of a config-5
+    # distribution (the weak-scaling base)
+    workload = os.environ.get("CAD_WORKLOAD", "cfg2")
+    if workload == "cfg2":
+        shape, lengths = CF.LLAMA8B, S.sample_batch(CF.length_dist("pretrain", SEED), 131072)
+        wl_name = CFG2_WORKLOAD
+    elif workload == "cfg4":
+        shape, lengths = CF.LLAMA34B, S.sample_batch(CF.length_dist("pretrain", SEED, max_doc_len=262144), 1 << 20)
+        wl_name = (f"BASELINE config 4: Llama-34B CA (64 Q / 8 KV heads, d=128), 1048576 packed tokens, "
+                   f"pretrain_upsampled docs up to 256K seed {SEED}, one layer fwd+bwd, one GPU")
+    elif workload == "cfg3":
+        shape, lengths = CF.LLAMA8B, S.sample_batch(CF.length_dist("pretrain", SEED), 65536)
+        wl_name = (f"BASELINE config 3 shape, one GPU's 65536 tokens (pretrain_upsampled seed {SEED}), "
+                   "Llama-3-8B CA, one layer fwd+bwd")
+    elif workload.startswith("cfg5-"):
+        shape, lengths = CF.LLAMA8B, S.sample_batch(CF.length_dist(workload[5:], SEED), 65536)
+        wl_name = (f"BASELINE config 5 ({workload[5:]}), one GPU's 65536 tokens, Llama-3-8B CA, seed {SEED}, "
+                   "one layer fwd+bwd")
+    else:
+        raise ValueError(f"unknown CAD_WORKLOAD {workload!r}")
     T = sum(lengths)
     tasks, off = [], 0
     for l in lengths:
@@ -362,9 +383,10 @@ def single_gpu(args):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": CFG2_WORKLOAD,
+        "config": {"workload": wl_name, "workload_id": workload,
                    "docs": lengths, "causal_pairs": plan.causal_pairs, "flops_per_step": flops["total"],
-                   "l2": "inputs larger than L2 (Q alone is 1 GiB)", "parallelism": "single GPU"},
+                   "l2": f"inputs larger than L2 (Q alone is {T * shape.h_q * 256 / 2**30:.2f} GiB)",
+                   "parallelism": "single GPU"},
         "per_gpu_tflops": value, "pct_bf16_peak": value / peak, "pct_bf16_peak_sustained": value / peak_sus,
         "tokens_per_s": T / (ms / 1e3),
         "imbalance": {"max_over_mean_pairs": 1.0, "max_over_mean_time": 1.0},
