@@ -65,7 +65,9 @@ def run(args, metric, load_peaks, ClockSampler):
         raise ValueError(f"unknown CAD_WORKLOAD {workload!r}")
     per_gpu = total // world
     lengths = S.sample_batch(dist_, total)
-    balance = os.environ.get("CAD_BALANCE_HALVES", "0") != "0"
+    # halves: 0 = the reference's assign_halves split, 1 = evened out per
+    # server, 2 = one half (no ping-pong)
+    balance = int(os.environ.get("CAD_BALANCE_HALVES", "0"))
     lp = D.LayerPlan(lengths, world, rank, shape, balance_halves=balance)
     layers = int(os.environ.get("CAD_LAYERS", "1" if workload == "cfg4" else "4"))
     dev = torch.device("cuda", local)
@@ -256,7 +258,7 @@ def run(args, metric, load_peaks, ClockSampler):
                                    f"ping-pong halves, {layers} stacked CA layer(s) fwd+bwd per step "
                                    "(identity between layers)",
                        "workload_id": workload, "layers_per_step": layers,
-                       "halves": "balanced per server" if balance else "reference assign_halves",
+                       "halves": ["reference assign_halves", "balanced per server", "one half (no ping-pong)"][balance],
                        "docs": len(lengths), "tasks": len(lp.plan.tasks), "migrations": lp.plan.migrations,
                        "flops_per_step": flops, "l2": "inputs larger than L2",
                        "parallelism": f"CA servers x{world} (scheduler sharding)", "transport": "ipc"},

@@ -382,9 +382,11 @@ typedef struct cad_xfer {
 int cad_layer_plan_create(const cad_plan* plan, const cad_item* home_items,
                           int64_t n_items, int32_t rank, int64_t q_row_bytes,
                           int64_t kv_row_bytes, cad_layer_plan** out);
-/* Same, with balance != 0: each server's halves evened out in causal pairs
+/* Same, with balance = 1: each server's halves evened out in causal pairs
  * (to within 1 %) by moving the query tail of the heavier half's largest
- * contiguous CA-task into the other half. The reference's halves
+ * contiguous CA-task into the other half; balance = 2: one half (every task
+ * in the ping half, the pong half empty: no ping-pong, half the launches,
+ * for batches whose transfers are negligible). The reference's halves
  * (assign_halves, P/src/sim.cpp:34-46) balance nothing per server; served
  * tasks, residency and results are unchanged, only the ping/pong split
  * moves. balance = 0 is cad_layer_plan_create. */
@@ -505,7 +507,9 @@ typedef struct cad_layer_cfg {
                             the identity between them (every layer sees the
                             step's inputs; O/LSE/dQ are the last layer's, dK/dV
                             the SUM over the L layers) */
-  int32_t balance_halves; /* 0: the reference's assign_halves split */
+  int32_t balance_halves; /* 0: the reference's assign_halves split; 1: halves
+                            evened out per server; 2: one half (see
+                            cad_layer_plan_create_ex) */
   int32_t reserve_sms;   /* CA kernels leave this many SMs free (NCCL) */
   int32_t pad_[2];
 } cad_layer_cfg;

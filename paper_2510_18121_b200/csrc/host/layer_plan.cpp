@@ -136,16 +136,18 @@ i64 part_pairs(const Part& p) { return cad::causal_pairs(p.qe - p.qb, p.kv); }
 // not per half; the halves of one server can differ several-fold (one long
 // document), and every half of every rank waits for its peers' previous
 // returns, so the per-half maximum over ranks sets the step time.
-std::vector<Part> server_parts(const cad::Plan& P, const cad::DevicePlan& dev, bool balance) {
+std::vector<Part> server_parts(const cad::Plan& P, const cad::DevicePlan& dev, int balance) {
   std::vector<Part> parts;
   for (const cad::Served& sv : dev.served) {
     const cad::Item& it = P.tasks[static_cast<size_t>(sv.task)].item;
     const bool ht = it.layout == cad::Layout::head_tail;
-    parts.push_back({sv.task, it.q_begin, it.q_end, it.q_end, sv.half, !ht});
+    // balance 2: one half (every task in the ping half; the pong half is empty)
+    const int half = balance == 2 ? 0 : sv.half;
+    parts.push_back({sv.task, it.q_begin, it.q_end, it.q_end, half, !ht});
     if (ht) parts.push_back({sv.task, it.ht_mirror - it.q_end, it.ht_mirror - it.q_begin,
-                             it.ht_mirror - it.q_begin, sv.half, false});
+                             it.ht_mirror - it.q_begin, half, false});
   }
-  if (!balance) return parts;
+  if (balance != 1) return parts;
   for (int round = 0; round < 4; ++round) {
     i64 load[2] = {0, 0};
     for (const Part& p : parts) load[p.half] += part_pairs(p);
@@ -221,7 +223,8 @@ int cad_layer_plan_create_ex(const cad_plan* plan, const cad_item* home_items, i
     L->world = world;
     L->home_rows = rows_of[static_cast<size_t>(rank)];
     std::vector<std::vector<Part>> parts_of;
-    for (int32_t s = 0; s < world; ++s) parts_of.push_back(server_parts(P, devs[static_cast<size_t>(s)], balance != 0));
+    if (balance < 0 || balance > 2) throw cad::DomainError("balance must be 0, 1 or 2");
+    for (int32_t s = 0; s < world; ++s) parts_of.push_back(server_parts(P, devs[static_cast<size_t>(s)], balance));
     for (int h = 0; h < 2; ++h) {
       Builder qd(world), kvd(world);
       std::vector<Half> all(static_cast<size_t>(world));  // server-side layouts of every rank

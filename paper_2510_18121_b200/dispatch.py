@@ -92,7 +92,7 @@ class LayerPlan:
         q_row = shape.h_q * shape.head_dim * 2
         kv_row = 2 * shape.h_kv * shape.head_dim * 2
         check(lib().cad_layer_plan_create_ex(ph.h, arr, len(self.home_items), rank, q_row, kv_row,
-                                             int(balance_halves), C.byref(lp)))
+                                             int(balance_halves), C.byref(lp)))  # 0/False, 1/True, or 2 (one half)
         try:
             self.halves: List[HalfPlan] = []
             for h in (0, 1):

@@ -18,12 +18,14 @@ SHAPE = CF.Shape("test", 2, 1)
     (4, [300, 300, 300, 300, 300, 300, 300, 300]),
     (8, [1400, 40, 100, 500, 60, 300, 200, 128, 72]),  # 8 ranks, one document over four
 ])
-@pytest.mark.parametrize("balance", [False, True])
+@pytest.mark.parametrize("balance", [0, 1, 2])  # reference halves, balanced halves, one half
 def test_distributed_layer_matches_whole_batch(world, lengths, balance):
     total = sum(lengths)
     assert total % world == 0
     out, ref, plans = run_layer(lengths, world, SHAPE, seed=world, balance_halves=balance)
     assert plans[0].plan.migrations > 0 or world == 4
+    if balance == 2:
+        assert all(not p.halves[1].tasks for p in plans)
     for r in range(world):
         for name, tol in (("o", 1e-5), ("lse", 1e-5), ("dq", 1e-4), ("dk", 1e-4), ("dv", 1e-4)):
             err = np.abs(out[name][r] - ref[name][r]).max()
