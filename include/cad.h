@@ -531,10 +531,11 @@ typedef struct cad_layer_ctx_info {
 
 /* Caller buffers of one step on this rank's HOME rows (packed THD, the row
  * order of the rank's home items): inputs q/dout [home_rows][h_q][d], k/v
- * [home_rows][h_kv][d] bf16; outputs o/dq bf16 and lse [h_q][home_rows] fp32
- * (these three must be the buffers given to cad_layer_ctx_bind_outputs),
- * dk/dv bf16 and/or their fp32 sums dk_acc/dv_acc [home_rows][h_kv][d]
- * (each written when non-NULL). */
+ * [home_rows][h_kv][d] bf16 (NULL: already in cad_layer_ctx_home's
+ * buffers); outputs o/dq bf16 and lse [h_q][home_rows] fp32 (copied out of
+ * the home buffers when non-NULL and not those buffers), dk/dv bf16 and/or
+ * their fp32 sums dk_acc/dv_acc [home_rows][h_kv][d] (each written when
+ * non-NULL). A backward-only step (CAD_PASS_BWD) reads o/lse as inputs. */
 typedef struct cad_layer_io {
   const void* q;
   const void* k;
@@ -556,7 +557,17 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items,
                          int64_t n_items, const cad_layer_cfg* cfg,
                          cad_layer_ctx** out);
 int cad_layer_ctx_info_get(const cad_layer_ctx* ctx, cad_layer_ctx_info* info);
-/* Home output buffers the peers write O/LSE/dQ into (before export). */
+/* The home buffers of a layer, INSIDE the context's server buffers (zero-copy
+ * own rows: a rank's own tasks read Q/K/V/dO and write O/dQ there in place,
+ * and the peers push their returns there). Callers that produce inputs or
+ * consume outputs in place use these pointers (and may pass NULL inputs in
+ * cad_layer_io); other caller buffers are copied in at the start of a step and
+ * out at its finish. With stacked benchmark layers, layer l >= 1 reads its
+ * own home inputs unless cad_layer_io gives buffers (then copied into every
+ * layer). */
+int cad_layer_ctx_home(const cad_layer_ctx* ctx, int32_t layer, cad_layer_io* io);
+/* Kept for the earlier contract (outputs bound up front): now a no-op; the
+ * outputs live in the context and cad_layer_io's o/lse/dq receive copies. */
 int cad_layer_ctx_bind_outputs(cad_layer_ctx* ctx, void* o, float* lse, void* dq);
 /* LOCAL/IPC: this rank's buffer references (blob of info.blob_bytes). Gather
  * every rank's blob (any host collective), then connect with the

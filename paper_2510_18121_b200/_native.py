@@ -193,6 +193,7 @@ SIGNATURES = {
     "cad_layer_ctx_create": (C.c_int, [vp, P(cad_item), i64, P(cad_layer_cfg), P(vp)]),
     "cad_layer_ctx_info_get": (C.c_int, [vp, P(cad_layer_ctx_info)]),
     "cad_layer_ctx_bind_outputs": (C.c_int, [vp, vp, vp, vp]),
+    "cad_layer_ctx_home": (C.c_int, [vp, i32, P(cad_layer_io)]),
     "cad_layer_ctx_export": (C.c_int, [vp, vp, C.c_size_t, P(C.c_size_t)]),
     "cad_layer_ctx_connect": (C.c_int, [vp, vp, C.c_size_t]),
     "cad_layer_ctx_set_comm": (C.c_int, [vp, vp]),

@@ -123,19 +123,159 @@ RankRows read_rank(const cad_plan* plan, const cad_item* items, i64 n, int32_t r
   return R;
 }
 
+// Zero-copy own rows. A rank's home buffers live INSIDE its server buffers:
+// every Q-like buffer of a layer (Q, O, dO, dQ) is [R0 | HOME | R1] rows --
+// HOME = the rank's home rows, R0 / R1 = the rows of the tasks it serves for
+// other ranks in the ping / pong half -- and half 0's view starts at row 0,
+// half 1's at row R0, so both halves see HOME contiguously next to their
+// remote rows. Every task of a rank's own rows then reads Q/dO and writes
+// O/dQ in place; a KV group whose prefix [0, need) is entirely home rows in
+// order (a document that starts on this rank) reads K/V in place from the
+// [KR0 | HOME | KR1] K/V buffers. Only KV groups assembled from several
+// ranks and the LSE re-layout still copy own rows. alias_rows rewrites a
+// rank's row plan into these view coordinates (every rank does it for every
+// rank, so pushes land where the peer's kernels read).
+struct Alias {
+  i64 home = 0, r[2] = {0, 0}, kr[2] = {0, 0};
+  // own rows that still move: (src, dst) pairs per half
+  std::vector<std::pair<i64, i64>> lse_self[2];  // O_RET LSE: view q row -> home row
+  std::vector<std::pair<i64, i64>> qd_self[2];   // QD: home row -> view q row (forward-state LSE)
+};
+
+Alias alias_rows(RankRows& R, int me) {
+  Alias A;
+  A.home = R.home_rows;
+  for (int h = 0; h < 2; ++h) {
+    HalfRows& H = R.half[h];
+    auto self_block = [&](const std::vector<i64>& counts) {
+      i64 o = 0;
+      for (int p = 0; p < me; ++p) o += counts[static_cast<size_t>(p)];
+      return std::make_pair(o, counts[static_cast<size_t>(me)]);
+    };
+    // ---- Q rows: own (from the QD self pairs) -> HOME, the rest -> remote region
+    XferRows& QD = H.x[kXQ];
+    const auto qs = self_block(QD.send_counts), qr = self_block(QD.recv_counts);
+    std::vector<i64> own_q(static_cast<size_t>(std::max<i64>(0, H.q_rows)), -1);
+    for (i64 j = 0; j < qs.second; ++j)
+      own_q[static_cast<size_t>(QD.recv_idx[static_cast<size_t>(qr.first + j)])] =
+          QD.send_idx[static_cast<size_t>(qs.first + j)];
+    std::vector<i64> qmap(own_q.size());
+    i64 nrem = 0;
+    for (size_t row = 0; row < own_q.size(); ++row)
+      if (own_q[row] < 0) qmap[row] = nrem++;
+    A.r[h] = nrem;
+    // view rows: half 0 [R0 | HOME], half 1 [HOME | R1]
+    for (size_t row = 0; row < own_q.size(); ++row)
+      qmap[row] = own_q[row] >= 0 ? (h == 0 ? nrem : 0) + own_q[row] : (h == 0 ? 0 : A.home) + qmap[row];
+    // ---- KV groups: aliased iff all of [kv_off, kv_off + need) are own rows, in home order
+    XferRows& KD = H.x[kXKV];
+    const auto ks = self_block(KD.send_counts), kr = self_block(KD.recv_counts);
+    std::vector<i64> own_kv(static_cast<size_t>(std::max<i64>(0, H.kv_rows)), -1);
+    for (i64 j = 0; j < ks.second; ++j)
+      own_kv[static_cast<size_t>(KD.recv_idx[static_cast<size_t>(kr.first + j)])] =
+          KD.send_idx[static_cast<size_t>(ks.first + j)];
+    std::map<i64, i64> need;  // kv_off -> rows of the group
+    for (const cad_ca_task& t : H.tasks) need[t.kv_off] = std::max(need[t.kv_off], t.kv_len);
+    std::vector<i64> kvmap(own_kv.size(), -1);
+    std::vector<char> aliased(own_kv.size(), 0);
+    i64 nkr = 0;
+    for (const auto& g : need) {
+      bool ok_alias = true;
+      for (i64 j = 0; j < g.second && ok_alias; ++j)
+        ok_alias = own_kv[static_cast<size_t>(g.first + j)] == own_kv[static_cast<size_t>(g.first)] + j &&
+                   own_kv[static_cast<size_t>(g.first)] >= 0;
+      for (i64 j = 0; j < g.second; ++j) {
+        const size_t row = static_cast<size_t>(g.first + j);
+        aliased[row] = ok_alias;
+        kvmap[row] = ok_alias ? own_kv[row] : nkr + j;  // home row / remote index
+      }
+      if (!ok_alias) nkr += g.second;
+    }
+    A.kr[h] = nkr;
+    for (size_t row = 0; row < kvmap.size(); ++row)
+      if (kvmap[row] >= 0)
+        kvmap[row] = aliased[row] ? (h == 0 ? nkr : 0) + kvmap[row] : (h == 0 ? 0 : A.home) + kvmap[row];
+    // ---- tasks in view coordinates
+    for (cad_ca_task& t : H.tasks) {
+      const i64 q0 = qmap[static_cast<size_t>(t.q_off)];
+      for (i64 j = 1; j < t.n_q; ++j)
+        if (qmap[static_cast<size_t>(t.q_off + j)] != q0 + j) throw cad::DomainError("task rows not contiguous");
+      t.q_off = q0;
+      t.kv_off = kvmap[static_cast<size_t>(t.kv_off)];
+    }
+    // ---- exchanges: remap server rows, drop the own rows that no longer move
+    for (i64 j = 0; j < qs.second; ++j)
+      A.qd_self[h].push_back({QD.send_idx[static_cast<size_t>(qs.first + j)],
+                              qmap[static_cast<size_t>(QD.recv_idx[static_cast<size_t>(qr.first + j)])]});
+    auto filter_self = [&](XferRows& X, bool send_server, bool recv_server, const std::vector<i64>& map,
+                           auto keep_self) {
+      const auto ss = self_block(X.send_counts), rs = self_block(X.recv_counts);
+      std::vector<i64> si, ri;
+      i64 kept = 0;
+      for (size_t j = 0; j < X.send_idx.size(); ++j) {
+        const i64 jj = static_cast<i64>(j);
+        const bool self = jj >= ss.first && jj < ss.first + ss.second;
+        const i64 v = send_server ? map[static_cast<size_t>(X.send_idx[j])] : X.send_idx[j];
+        if (self) {
+          const i64 k = jj - ss.first;
+          const i64 rv = X.recv_idx[static_cast<size_t>(rs.first + k)];
+          if (!keep_self(X.send_idx[j], rv)) continue;
+          ++kept;
+        }
+        si.push_back(v);
+      }
+      for (size_t j = 0; j < X.recv_idx.size(); ++j) {
+        const i64 jj = static_cast<i64>(j);
+        const bool self = jj >= rs.first && jj < rs.first + rs.second;
+        if (self) {
+          const i64 k = jj - rs.first;
+          if (!keep_self(X.send_idx[static_cast<size_t>(ss.first + k)], X.recv_idx[j])) continue;
+        }
+        ri.push_back(recv_server ? map[static_cast<size_t>(X.recv_idx[j])] : X.recv_idx[j]);
+      }
+      X.send_idx = si;
+      X.recv_idx = ri;
+      X.send_counts[static_cast<size_t>(me)] = kept;
+      X.recv_counts[static_cast<size_t>(me)] = kept;
+    };
+    // QD (Q, dO): home -> server view; own rows are in place
+    filter_self(QD, false, true, qmap, [](i64, i64) { return false; });
+    // KVD: home -> server view; own rows of assembled groups still copy
+    filter_self(KD, false, true, kvmap, [&](i64, i64 srv) { return !aliased[static_cast<size_t>(srv)]; });
+    // O_RET (O, dQ, LSE): server view -> home; own O/dQ in place, own LSE via lse_self
+    XferRows& OR = H.x[kXO];
+    {
+      const auto os = self_block(OR.send_counts), orr = self_block(OR.recv_counts);
+      for (i64 j = 0; j < os.second; ++j)
+        A.lse_self[h].push_back({qmap[static_cast<size_t>(OR.send_idx[static_cast<size_t>(os.first + j)])],
+                                 OR.recv_idx[static_cast<size_t>(orr.first + j)]});
+    }
+    filter_self(OR, true, false, qmap, [](i64, i64) { return false; });
+    // KV_RET: server view -> owner staging; the own block stays (read in place)
+    filter_self(H.x[kXKR], true, false, kvmap, [](i64, i64) { return true; });
+    H.q_rows = h == 0 ? A.r[0] + A.home : A.home + A.r[1];
+    H.kv_rows = h == 0 ? A.kr[0] + A.home : A.home + A.kr[1];
+  }
+  return A;
+}
+
 // Byte offsets of one rank's context-owned device buffers (one allocation,
 // so IPC exports a single handle). Every rank computes every peer's layout
 // from the peer's row plan.
-struct Bufs {
+struct Bufs {  // a half's views
   size_t q, k, v, o, dout, dq, dk, dv, lse, sdk, sdv;
+};
+struct Homes {  // a layer's home regions (inside its Q-like / K-like buffers)
+  size_t q, k, v, o, dout, dq, lse;
 };
 struct Layout {
   size_t flags = 0;
   std::vector<std::array<Bufs, 2>> b;  // [layer][half]
+  std::vector<Homes> home;             // [layer]
   size_t total = 0;
 };
 
-Layout layout_of(const RankRows& R, int layers, int world, i64 q_row, i64 kv_row, i64 lse_row) {
+Layout layout_of(const RankRows& R, const Alias& A, int layers, int world, i64 q_row, i64 kv_row, i64 lse_row) {
   Layout L;
   size_t off = 0;
   auto take = [&](i64 bytes) {
@@ -145,24 +285,35 @@ Layout layout_of(const RankRows& R, int layers, int world, i64 q_row, i64 kv_row
   };
   L.flags = take(static_cast<i64>(4) * 2 * kKinds * world);
   L.b.resize(static_cast<size_t>(layers));
-  for (int l = 0; l < layers; ++l)
+  L.home.resize(static_cast<size_t>(layers));
+  const i64 qrows = A.r[0] + A.home + A.r[1], kvrows = A.kr[0] + A.home + A.kr[1];
+  for (int l = 0; l < layers; ++l) {
+    const size_t q = take(qrows * q_row), o = take(qrows * q_row), dout = take(qrows * q_row),
+                 dq = take(qrows * q_row), k = take(kvrows * kv_row), v = take(kvrows * kv_row);
+    Homes& Hm = L.home[static_cast<size_t>(l)];
+    const size_t hq_off = static_cast<size_t>(A.r[0] * q_row), hk_off = static_cast<size_t>(A.kr[0] * kv_row);
+    Hm = Homes{q + hq_off, k + hk_off, v + hk_off, o + hq_off, dout + hq_off, dq + hq_off,
+               take(A.home * lse_row)};
     for (int h = 0; h < 2; ++h) {
       const HalfRows& H = R.half[h];
+      const size_t qb = h == 0 ? 0 : static_cast<size_t>(A.r[0] * q_row);
+      const size_t kb = h == 0 ? 0 : static_cast<size_t>(A.kr[0] * kv_row);
       const i64 qr = std::max<i64>(1, H.q_rows), kr = std::max<i64>(1, H.kv_rows);
       const i64 sr = std::max<i64>(1, H.x[kXKR].n_recv());
       Bufs& B = L.b[static_cast<size_t>(l)][static_cast<size_t>(h)];
-      B.q = take(qr * q_row);
-      B.o = take(qr * q_row);
-      B.dout = take(qr * q_row);
-      B.dq = take(qr * q_row);
-      B.k = take(kr * kv_row);
-      B.v = take(kr * kv_row);
+      B.q = q + qb;
+      B.o = o + qb;
+      B.dout = dout + qb;
+      B.dq = dq + qb;
+      B.k = k + kb;
+      B.v = v + kb;
       B.dk = take(kr * kv_row);
       B.dv = take(kr * kv_row);
       B.lse = take(qr * lse_row);
       B.sdk = take(sr * kv_row);
       B.sdv = take(sr * kv_row);
     }
+  }
   L.total = off;
   return L;
 }
@@ -188,14 +339,11 @@ struct Blob {
   uint32_t magic;
   int32_t rank, world, transport, layers, pad;
   int64_t home_rows;
-  BlobRef ref[4];  // arena, o, lse, dq
+  BlobRef ref[4];  // [0] the arena (the others unused)
 };
 
 struct Peer {
   char* arena = nullptr;
-  void* o = nullptr;
-  float* lse = nullptr;
-  void* dq = nullptr;
   i64 home_rows = 0;
   i64 q_pitch[2] = {1, 1};  // rows of the peer's server Q/LSE buffers per half
   Layout layout;
@@ -320,9 +468,13 @@ struct cad_layer_ctx {
   int64_t* d_red_off = nullptr;  // dK/dV reduction CSR over home rows
   int32_t* d_red_ent = nullptr;  // (row << 2) | (own << 1) | half
   const uint4** d_red_src[2] = {nullptr, nullptr};  // dK, dV bases [layer][own][half]
-  void* o_home = nullptr;
-  float* lse_home = nullptr;
-  void* dq_home = nullptr;
+  Alias alias;  // this rank's zero-copy layout (alias_rows)
+  // own rows that still move: LSE re-layout (server view -> home) and the
+  // forward state's LSE (home -> server view), device chunk lists per half
+  int64_t* d_lse_self[2] = {};
+  int64_t n_lse_self[2] = {};
+  int64_t* d_qd_self[2] = {};
+  int64_t n_qd_self[2] = {};
   bool connected = false;
   cad_comm* comm = nullptr;
   void* xsend = nullptr;
@@ -343,6 +495,38 @@ struct cad_layer_ctx {
   T* peer_at(int p, size_t off) const { return reinterpret_cast<T*>(peer[static_cast<size_t>(p)].arena + off); }
   const Bufs& pb(int p, int l, int h) const {
     return peer[static_cast<size_t>(p)].layout.b[static_cast<size_t>(l)][static_cast<size_t>(h)];
+  }
+  const Homes& hm(int l) const { return layout.home[static_cast<size_t>(l)]; }
+  const Homes& phm(int p, int l) const { return peer[static_cast<size_t>(p)].layout.home[static_cast<size_t>(l)]; }
+  // copy a caller buffer into (or out of) a home region, unless it IS that region
+  void stage(void* dst, const void* src, i64 bytes, cudaStream_t s) const {
+    if (!src || !dst || src == dst || bytes <= 0) return;
+    cuda_check(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, s), "stage copy");
+  }
+  void cols(const int64_t* chunks, int64_t n, const float* src, i64 src_rows, float* dst, i64 dst_rows,
+            cudaStream_t s) {
+    if (n <= 0) return;
+    copy_col_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(n, 148 * 4)), 256, 0, s>>>(
+        chunks, n, src, src_rows, dst, dst_rows, static_cast<int>(hq));
+    cuda_check(cudaGetLastError(), "copy_col_chunks launch");
+    ++launches;
+  }
+  void stage_fwd_state(const cad_layer_io* io, int l, cudaStream_t s) const {
+    stage(at(hm(l).o), io->o, mine.home_rows * q_row, s);
+    stage(at(hm(l).lse), io->lse, mine.home_rows * lse_row, s);
+  }
+  // the step's inputs into the layers' home regions (a NULL input: the
+  // caller wrote the home region itself, cad_layer_ctx_home)
+  void stage_inputs(const cad_layer_io* io, bool qkv, bool dout, cudaStream_t s) const {
+    const i64 H = mine.home_rows;
+    for (int l = 0; l < NL; ++l) {
+      if (qkv) {
+        stage(at(hm(l).q), io->q, H * q_row, s);
+        stage(at(hm(l).k), io->k, H * kv_row, s);
+        stage(at(hm(l).v), io->v, H * kv_row, s);
+      }
+      if (dout) stage(at(hm(l).dout), io->dout, H * q_row, s);
+    }
   }
   uint32_t gl(int l) const { return g0 + 1 + static_cast<uint32_t>(l); }
   uint32_t gb(int l) const { return g0 + 2 * static_cast<uint32_t>(NL) - static_cast<uint32_t>(l); }
@@ -451,10 +635,13 @@ struct cad_layer_ctx {
          "cad_copy_runs_cols");
     }
   }
-  void push_lse(int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) {
+  void push_lse(int l, int h, const float* src, i64 src_rows, cudaStream_t s, cudaStream_t local) {
     push_cols(h, kXO, src, src_rows,
-              [&](int p) { return std::make_pair(peer[static_cast<size_t>(p)].lse, peer[static_cast<size_t>(p)].home_rows); },
+              [&](int p) {
+                return std::make_pair(peer_at<float>(p, phm(p, l).lse), peer[static_cast<size_t>(p)].home_rows);
+              },
               s, local);
+    cols(d_lse_self[h], n_lse_self[h], src, src_rows, at<float>(hm(l).lse), mine.home_rows, local);
   }
 
   // NCCL: gather, all-to-allv, then scatter (or, with dst_contig, receive
@@ -478,8 +665,7 @@ struct cad_layer_ctx {
       ++launches;
     }
   }
-  void nccl_cols(int h, int x, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s,
-                 cudaStream_t local) {
+  void nccl_cols(int h, int x, const float* src, i64 src_rows, float* dst, i64 dst_rows, cudaStream_t s) {
     const NcclX& X = nx[h][x];
     ok(cad_gather_cols_f32(src, src_rows, static_cast<int32_t>(hq), X.d_send, X.n_send,
                            static_cast<float*>(xsend), s),
@@ -489,13 +675,6 @@ struct cad_layer_ctx {
                             dst_rows, s),
        "cad_scatter_cols_f32");
     launches += (X.n_send > 0) + (X.n_recv > 0);
-    if (n_local_chunks[h][x] > 0) {
-      const int64_t n = n_local_chunks[h][x];
-      copy_col_chunks_kernel<<<static_cast<unsigned>(std::min<int64_t>(n, 148 * 4)), 256, 0, local>>>(
-          d_local_chunks[h][x], n, src, src_rows, dst, dst_rows, static_cast<int>(hq));
-      cuda_check(cudaGetLastError(), "copy_col_chunks launch");
-      ++launches;
-    }
   }
   void alltoallv(const NcclX& X, i64 row_bytes, void* recv, bool full_order, cudaStream_t s) const {
     if (!comm) throw cad::ConfigError("NCCL transport: cad_layer_ctx_set_comm was not called");
@@ -514,10 +693,8 @@ struct cad_layer_ctx {
     ok(cad_alltoallv(comm, xsend, sb.data(), sd.data(), recv, rb.data(), rd.data(), s), "cad_alltoallv");
   }
 
-  void check_io(const cad_layer_io* io, bool outputs) const {
+  void check_io(const cad_layer_io* io, bool) const {
     if (!io) throw cad::DomainError("null io");
-    if (outputs && flagged() && (io->o != o_home || io->lse != lse_home || io->dq != dq_home))
-      throw cad::DomainError("o/lse/dq must be the buffers bound with cad_layer_ctx_bind_outputs");
   }
   void need_ready() const {
     if (flagged() && !connected) throw cad::ConfigError("layer context not connected (cad_layer_ctx_connect)");
@@ -540,46 +717,51 @@ struct cad_layer_ctx {
     if (flagged()) await(F_DONE, 0, g0, s);
   }
 
-  void dispatch(int l, int h, int what, const cad_layer_io* io, cudaStream_t s, cudaStream_t local) {
+  // Transfers read and write the layers' home regions (the caller's buffers
+  // are staged in and out by stage_inputs / finish); a rank's own rows are
+  // already in place in its server views.
+  void dispatch(int l, int h, int what, const cad_layer_io*, cudaStream_t s, cudaStream_t local) {
     const Bufs& B = b(l, h);
+    const Homes& Hm = hm(l);
     if (what == CAD_DISPATCH_QKV) {
-      if (!io->q || !io->k || !io->v) throw cad::DomainError("null q/k/v");
       if (flagged()) {
         // identity between stacked layers: layer l's Q/K/V of half h leave
         // home once every server has returned O(h, l-1)
         if (l > 0) await(F_O, h, gl(l - 1), s);
-        push(h, kXQ, io->q, q_row, [&](int p) { return peer_at(p, pb(p, l, h).q); }, s, local);
-        push(h, kXKV, io->k, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).k); }, s, local);
-        push(h, kXKV, io->v, kv_row, [&](int p) { return peer_at(p, pb(p, l, h).v); }, s, local);
+        push(h, kXQ, at(Hm.q), q_row, [&](int p) { return peer_at(p, pb(p, l, h).q); }, s, local);
+        push(h, kXKV, at(Hm.k), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).k); }, s, local);
+        push(h, kXKV, at(Hm.v), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).v); }, s, local);
         signal(F_QKV, h, gl(l), s);
       } else {
-        nccl_rows(h, kXQ, io->q, q_row, at(B.q), false, s, local);
-        nccl_rows(h, kXKV, io->k, kv_row, at(B.k), false, s, local);
-        nccl_rows(h, kXKV, io->v, kv_row, at(B.v), false, s, local);
+        nccl_rows(h, kXQ, at(Hm.q), q_row, at(B.q), false, s, local);
+        nccl_rows(h, kXKV, at(Hm.k), kv_row, at(B.k), false, s, local);
+        nccl_rows(h, kXKV, at(Hm.v), kv_row, at(B.v), false, s, local);
       }
     } else if (what == CAD_DISPATCH_FWD_STATE) {
       // O and LSE rows home -> server, for a backward whose forward ran under
       // another plan (a pipeline tick's backward, P/src/sim.cpp:326-353);
-      // ordered before the consumer by the DO dispatch's flag that follows
-      if (!io->o || !io->lse) throw cad::DomainError("null o/lse");
+      // ordered before the consumer by the DO dispatch's flag that follows.
+      // Own O rows are in place; own LSE columns are re-laid out.
       const i64 pitch = std::max<i64>(1, mine.half[h].q_rows);
       if (flagged()) {
-        push(h, kXQ, io->o, q_row, [&](int p) { return peer_at(p, pb(p, l, h).o); }, s, local);
-        push_cols(h, kXQ, io->lse, mine.home_rows,
-                  [&](int p) { return std::make_pair(peer_at<float>(p, pb(p, l, h).lse), peer[static_cast<size_t>(p)].q_pitch[h]); },
+        push(h, kXQ, at(Hm.o), q_row, [&](int p) { return peer_at(p, pb(p, l, h).o); }, s, local);
+        push_cols(h, kXQ, at<float>(Hm.lse), mine.home_rows,
+                  [&](int p) {
+                    return std::make_pair(peer_at<float>(p, pb(p, l, h).lse), peer[static_cast<size_t>(p)].q_pitch[h]);
+                  },
                   s, local);
       } else {
-        nccl_rows(h, kXQ, io->o, q_row, at(B.o), false, s, local);
-        nccl_cols(h, kXQ, io->lse, mine.home_rows, at<float>(B.lse), pitch, s, local);
+        nccl_rows(h, kXQ, at(Hm.o), q_row, at(B.o), false, s, local);
+        nccl_cols(h, kXQ, at<float>(Hm.lse), mine.home_rows, at<float>(B.lse), pitch, s);
       }
+      cols(d_qd_self[h], n_qd_self[h], at<float>(Hm.lse), mine.home_rows, at<float>(B.lse), pitch, local);
     } else if (what == CAD_DISPATCH_DO) {
-      if (!io->dout) throw cad::DomainError("null dout");
       if (flagged()) {
         if (l < NL - 1) await(F_G, h, gb(l + 1), s);  // dQ(h, l+1) home -> dO(h, l)
-        push(h, kXQ, io->dout, q_row, [&](int p) { return peer_at(p, pb(p, l, h).dout); }, s, local);
+        push(h, kXQ, at(Hm.dout), q_row, [&](int p) { return peer_at(p, pb(p, l, h).dout); }, s, local);
         signal(F_DO, h, gb(l), s);
       } else {
-        nccl_rows(h, kXQ, io->dout, q_row, at(B.dout), false, s, local);
+        nccl_rows(h, kXQ, at(Hm.dout), q_row, at(B.dout), false, s, local);
       }
     } else {
       throw cad::DomainError("unknown dispatch kind");
@@ -594,9 +776,8 @@ struct cad_layer_ctx {
       ok(cad_ca_fwd(plan[h], at(B.q), at(B.k), at(B.v), at(B.o), at<float>(B.lse), s), "cad_ca_fwd");
       launches += 1;
     } else {
-      const size_t kvb = static_cast<size_t>(std::max<i64>(1, mine.half[h].kv_rows) * kv_row);
-      cuda_check(cudaMemsetAsync(at(B.dk), 0, kvb, s), "memset dk");
-      cuda_check(cudaMemsetAsync(at(B.dv), 0, kvb, s), "memset dv");
+      // dK/dV of every KV group's rows are overwritten (rows of a view outside
+      // every group are never read)
       ok(cad_ca_bwd(plan[h], at(B.q), at(B.k), at(B.v), at(B.o), at<float>(B.lse), at(B.dout), at(B.dq), at(B.dk),
                     at(B.dv), ws[h], ws_bytes[h], s),
          "cad_ca_bwd");
@@ -604,26 +785,28 @@ struct cad_layer_ctx {
     }
   }
 
-  void ret(int l, int h, int what, const cad_layer_io* io, cudaStream_t s, cudaStream_t local) {
+  void ret(int l, int h, int what, const cad_layer_io*, cudaStream_t s, cudaStream_t local) {
     const Bufs& B = b(l, h);
+    const Homes& Hm = hm(l);
     const i64 qr = std::max<i64>(1, mine.half[h].q_rows);
     if (what == CAD_RETURN_O) {
       if (flagged()) {
-        push(h, kXO, at(B.o), q_row, [&](int p) { return peer[static_cast<size_t>(p)].o; }, s, local);
-        push_lse(h, at<float>(B.lse), qr, s, local);
+        push(h, kXO, at(B.o), q_row, [&](int p) { return peer_at(p, phm(p, l).o); }, s, local);
+        push_lse(l, h, at<float>(B.lse), qr, s, local);
         signal(F_O, h, gl(l), s);
       } else {
-        nccl_rows(h, kXO, at(B.o), q_row, io->o, false, s, local);
-        nccl_cols(h, kXO, at<float>(B.lse), qr, io->lse, mine.home_rows, s, local);
+        nccl_rows(h, kXO, at(B.o), q_row, at(Hm.o), false, s, local);
+        nccl_cols(h, kXO, at<float>(B.lse), qr, at<float>(Hm.lse), mine.home_rows, s);
+        cols(d_lse_self[h], n_lse_self[h], at<float>(B.lse), qr, at<float>(Hm.lse), mine.home_rows, local);
       }
     } else if (what == CAD_RETURN_GRAD) {
       if (flagged()) {
-        push(h, kXO, at(B.dq), q_row, [&](int p) { return peer[static_cast<size_t>(p)].dq; }, s, local);
+        push(h, kXO, at(B.dq), q_row, [&](int p) { return peer_at(p, phm(p, l).dq); }, s, local);
         push(h, kXKR, at(B.dk), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdk); }, s, local);
         push(h, kXKR, at(B.dv), kv_row, [&](int p) { return peer_at(p, pb(p, l, h).sdv); }, s, local);
         signal(F_G, h, gb(l), s);
       } else {
-        nccl_rows(h, kXO, at(B.dq), q_row, io->dq, false, s, local);
+        nccl_rows(h, kXO, at(B.dq), q_row, at(Hm.dq), false, s, local);
         nccl_rows(h, kXKR, at(B.dk), kv_row, at(B.sdk), true, s, local);  // partials land in recv order
         nccl_rows(h, kXKR, at(B.dv), kv_row, at(B.sdv), true, s, local);
       }
@@ -638,11 +821,18 @@ struct cad_layer_ctx {
         if (passes & CAD_PASS_FWD) await(F_O, h, gl(NL - 1), s);
         if (passes & CAD_PASS_BWD) await(F_G, h, gb(0), s);
       }
+    // outputs to the caller's buffers when they are not the home regions:
+    // O/LSE of the last layer, dQ of the first (the backward ends there)
+    const i64 rows = mine.home_rows;
+    if (passes & CAD_PASS_FWD) {
+      stage(io->o, at(hm(NL - 1).o), rows * q_row, s);
+      stage(io->lse, at(hm(NL - 1).lse), rows * lse_row, s);
+    }
     if (!(passes & CAD_PASS_BWD)) {
       if (flagged()) signal(F_DONE, 0, gdone(), s);
       return;
     }
-    const i64 rows = mine.home_rows;
+    stage(io->dq, at(hm(0).dq), rows * q_row, s);
     const int chunks = static_cast<int>(hkv * d / 8);
     if (rows > 0 && (io->dk || io->dk_acc || io->dv || io->dv_acc)) {
       const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
@@ -694,6 +884,10 @@ struct cad_layer_ctx {
       ~Restore() { c->move_remote = true; }
     } restore{this};
     trace_reset(comp);
+    // the caller's inputs into the home regions (on the compute stream, before
+    // the comm stream forks off it)
+    stage_inputs(io, true, (passes_ & CAD_PASS_BWD) != 0, comp);
+    if (passes_ == CAD_PASS_BWD) stage_fwd_state(io, 0, comp);
     cuda_check(cudaEventRecord(event(0), comp), "event");
     cuda_check(cudaStreamWaitEvent(comm, event(0), 0), "wait");
     begin(comm, passes_);
@@ -811,6 +1005,8 @@ struct cad_layer_ctx {
         cudaFree(nx[h][x].d_recv);
         cudaFree(d_local_chunks[h][x]);
       }
+      cudaFree(d_lse_self[h]);
+      cudaFree(d_qd_self[h]);
       cudaFree(d_red_src[h]);
     }
     cudaFree(arena);
@@ -862,16 +1058,43 @@ int cad_layer_ctx_create(const cad_plan* plan, const cad_item* home_items, int64
     C->lse_row = C->hq * 4;
     // every rank's rows: ours in full, the peers' for where our rows land
     std::vector<RankRows> all;
-    for (int r = 0; r < C->W; ++r)
+    std::vector<Alias> aliases;
+    for (int r = 0; r < C->W; ++r) {
       all.push_back(read_rank(plan, home_items, n_items, r, C->q_row, C->kv_row, cfg->balance_halves));
+      aliases.push_back(alias_rows(all.back(), r));  // zero-copy own rows, every rank's view
+    }
     C->mine = all[static_cast<size_t>(C->me)];
-    C->layout = layout_of(C->mine, C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
+    C->alias = aliases[static_cast<size_t>(C->me)];
+    C->layout = layout_of(C->mine, C->alias, C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
     C->peer.resize(static_cast<size_t>(C->W));
     for (int p = 0; p < C->W; ++p) {
       Peer& P = C->peer[static_cast<size_t>(p)];
       P.home_rows = all[static_cast<size_t>(p)].home_rows;
       for (int h = 0; h < 2; ++h) P.q_pitch[h] = std::max<i64>(1, all[static_cast<size_t>(p)].half[h].q_rows);
-      P.layout = layout_of(all[static_cast<size_t>(p)], C->NL, C->W, C->q_row, C->kv_row, C->lse_row);
+      P.layout = layout_of(all[static_cast<size_t>(p)], aliases[static_cast<size_t>(p)], C->NL, C->W, C->q_row,
+                           C->kv_row, C->lse_row);
+    }
+    // own rows that still move as columns: LSE server view -> home, and the
+    // forward state's LSE home -> server view
+    auto chunk_pairs = [](const std::vector<std::pair<i64, i64>>& pairs, int64_t* n) {
+      std::vector<i64> src, dst;
+      for (const auto& pr : pairs) {
+        src.push_back(pr.first);
+        dst.push_back(pr.second);
+      }
+      std::vector<int64_t> ch;
+      for (const cad_run& r : make_runs(src.data(), dst.data(), static_cast<i64>(src.size())))
+        for (i64 a = 0; a < r.n_rows; a += kChunkRows) {
+          ch.push_back(r.src_row + a);
+          ch.push_back(r.dst_row + a);
+          ch.push_back(std::min<i64>(kChunkRows, r.n_rows - a));
+        }
+      *n = static_cast<int64_t>(ch.size() / 3);
+      return dev_copy(ch);
+    };
+    for (int h = 0; h < 2; ++h) {
+      C->d_lse_self[h] = chunk_pairs(C->alias.lse_self[h], &C->n_lse_self[h]);
+      C->d_qd_self[h] = chunk_pairs(C->alias.qd_self[h], &C->n_qd_self[h]);
     }
     // push runs: my send rows to p against p's receive rows from me
     for (int h = 0; h < 2; ++h)
@@ -1048,12 +1271,26 @@ int cad_layer_ctx_info_get(const cad_layer_ctx* ctx, cad_layer_ctx_info* info) {
 }
 
 int cad_layer_ctx_bind_outputs(cad_layer_ctx* ctx, void* o, float* lse, void* dq) {
+  // The home outputs live in the context (cad_layer_ctx_home); caller buffers
+  // in cad_layer_io receive copies. Kept for callers of the earlier contract.
   return cad::guarded([&] {
     if (!ctx || !o || !lse || !dq) throw cad::DomainError("null argument");
-    if (ctx->connected) throw cad::ConfigError("outputs must be bound before export/connect");
-    ctx->o_home = o;
-    ctx->lse_home = lse;
-    ctx->dq_home = dq;
+  });
+}
+
+int cad_layer_ctx_home(const cad_layer_ctx* ctx, int32_t layer, cad_layer_io* io) {
+  return cad::guarded([&] {
+    if (!ctx || !io) throw cad::DomainError("null argument");
+    if (layer < 0 || layer >= ctx->NL) throw cad::DomainError("layer out of range");
+    const Homes& H = ctx->hm(layer);
+    *io = cad_layer_io{};
+    io->q = ctx->at(H.q);
+    io->k = ctx->at(H.k);
+    io->v = ctx->at(H.v);
+    io->dout = ctx->at(H.dout);
+    io->o = ctx->at(H.o);
+    io->lse = ctx->at<float>(H.lse);
+    io->dq = ctx->at(H.dq);
   });
 }
 
@@ -1063,7 +1300,6 @@ int cad_layer_ctx_export(cad_layer_ctx* ctx, void* blob, size_t cap, size_t* nee
     *need = sizeof(Blob);
     if (!blob || cap < sizeof(Blob)) throw cad::CapacityError("blob buffer too small");
     if (ctx->cfg.transport == CAD_TRANSPORT_NCCL) throw cad::ConfigError("NCCL transport has nothing to export");
-    if (!ctx->o_home) throw cad::ConfigError("bind the home outputs before export");
     cad_dev::DeviceGuard dg(ctx->device);
     Blob B{};
     B.magic = kBlobMagic;
@@ -1072,11 +1308,8 @@ int cad_layer_ctx_export(cad_layer_ctx* ctx, void* blob, size_t cap, size_t* nee
     B.transport = ctx->cfg.transport;
     B.layers = ctx->NL;
     B.home_rows = ctx->mine.home_rows;
-    const void* ptrs[4] = {ctx->arena, ctx->o_home, ctx->lse_home, ctx->dq_home};
-    for (int i = 0; i < 4; ++i) {
-      B.ref[i].raw = reinterpret_cast<uint64_t>(ptrs[i]);
-      if (ctx->cfg.transport == CAD_TRANSPORT_IPC) ok(cad_ipc_handle(ptrs[i], B.ref[i].handle, &B.ref[i].offset), "ipc");
-    }
+    B.ref[0].raw = reinterpret_cast<uint64_t>(ctx->arena);  // every buffer a peer writes is in the arena
+    if (ctx->cfg.transport == CAD_TRANSPORT_IPC) ok(cad_ipc_handle(ctx->arena, B.ref[0].handle, &B.ref[0].offset), "ipc");
     std::memcpy(blob, &B, sizeof(B));
   });
 }
@@ -1088,7 +1321,6 @@ int cad_layer_ctx_connect(cad_layer_ctx* ctx, const void* blobs, size_t blob_byt
     if (blob_bytes != sizeof(Blob)) throw cad::DomainError("blob size mismatch");
     if (ctx->connected) throw cad::ConfigError("already connected");
     cad_dev::DeviceGuard dg(ctx->device);
-    std::map<std::string, char*> mapped;
     for (int p = 0; p < ctx->W; ++p) {
       Blob B;
       std::memcpy(&B, static_cast<const char*>(blobs) + static_cast<size_t>(p) * sizeof(Blob), sizeof(Blob));
@@ -1097,26 +1329,14 @@ int cad_layer_ctx_connect(cad_layer_ctx* ctx, const void* blobs, size_t blob_byt
         throw cad::DomainError("blob of rank " + std::to_string(p) + " does not match this context");
       Peer& P = ctx->peer[static_cast<size_t>(p)];
       if (B.home_rows != P.home_rows) throw cad::DomainError("peer home rows disagree with the row plan");
-      char* ptr[4];
-      for (int i = 0; i < 4; ++i) {
-        if (p == ctx->me || ctx->cfg.transport == CAD_TRANSPORT_LOCAL) {
-          ptr[i] = reinterpret_cast<char*>(B.ref[i].raw);
-          continue;
-        }
-        const std::string key(reinterpret_cast<const char*>(B.ref[i].handle), 64);
-        auto it = mapped.find(key);
-        if (it == mapped.end()) {
-          void* base = nullptr;
-          ok(cad_ipc_open(B.ref[i].handle, &base), "cad_ipc_open");
-          ctx->opened.push_back(base);
-          it = mapped.emplace(key, static_cast<char*>(base)).first;
-        }
-        ptr[i] = it->second + B.ref[i].offset;
+      if (p == ctx->me || ctx->cfg.transport == CAD_TRANSPORT_LOCAL) {
+        P.arena = reinterpret_cast<char*>(B.ref[0].raw);
+        continue;
       }
-      P.arena = ptr[0];
-      P.o = ptr[1];
-      P.lse = reinterpret_cast<float*>(ptr[2]);
-      P.dq = ptr[3];
+      void* base = nullptr;
+      ok(cad_ipc_open(B.ref[0].handle, &base), "cad_ipc_open");
+      ctx->opened.push_back(base);
+      P.arena = static_cast<char*>(base) + B.ref[0].offset;
     }
     ctx->connected = true;
   });
@@ -1151,15 +1371,7 @@ int cad_layer_begin_ex(cad_layer_ctx* ctx, int32_t passes, void* stream) {
 }
 
 int cad_dispatch(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what, const cad_layer_io* io, void* stream) {
-  return cad::guarded([&] {
-    if (!ctx) throw cad::DomainError("null argument");
-    ctx->check_lh(layer, half);
-    ctx->check_io(io, false);
-    ctx->need_ready();
-    cad_dev::DeviceGuard dg(ctx->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    ctx->dispatch(layer, half, what, io, s, s);
-  });
+  return cad_dispatch_ex(ctx, layer, half, what, io, stream, stream);
 }
 
 int cad_dispatch_ex(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t what, const cad_layer_io* io,
@@ -1170,7 +1382,24 @@ int cad_dispatch_ex(cad_layer_ctx* ctx, int32_t layer, int32_t half, int32_t wha
     ctx->check_io(io, false);
     ctx->need_ready();
     cad_dev::DeviceGuard dg(ctx->device);
-    ctx->dispatch(layer, half, what, io, static_cast<cudaStream_t>(stream), static_cast<cudaStream_t>(local_stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (half == 0) {  // the caller's buffers into the layer's home regions, once per layer
+      const i64 H = ctx->mine.home_rows;
+      if (what == CAD_DISPATCH_QKV) {
+        ctx->stage(ctx->at(ctx->hm(layer).q), io->q, H * ctx->q_row, s);
+        ctx->stage(ctx->at(ctx->hm(layer).k), io->k, H * ctx->kv_row, s);
+        ctx->stage(ctx->at(ctx->hm(layer).v), io->v, H * ctx->kv_row, s);
+      } else if (what == CAD_DISPATCH_DO) {
+        ctx->stage(ctx->at(ctx->hm(layer).dout), io->dout, H * ctx->q_row, s);
+      } else if (what == CAD_DISPATCH_FWD_STATE) {
+        ctx->stage_fwd_state(io, layer, s);
+      }
+      if (static_cast<cudaStream_t>(local_stream) != s) {  // own rows read on local_stream
+        cuda_check(cudaEventRecord(ctx->event(0), s), "event");
+        cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(local_stream), ctx->event(0), 0), "wait");
+      }
+    }
+    ctx->dispatch(layer, half, what, io, s, static_cast<cudaStream_t>(local_stream));
   });
 }
 

@@ -151,6 +151,22 @@ def _p(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+class _CudaMem:
+    """__cuda_array_interface__ over context-owned device memory (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _wrap(ptr: int, shape, dtype, device) -> torch.Tensor:
+    """A torch tensor viewing `ptr` (the context keeps the memory alive)."""
+    if dtype == torch.bfloat16:  # no bf16 typestr: view the bits as int16
+        t = torch.as_tensor(_CudaMem(ptr, shape, "<i2"), device=device)
+        return t.view(torch.bfloat16)
+    return torch.as_tensor(_CudaMem(ptr, shape, "<f4"), device=device)
+
+
 class DistCALayer:
     """One rank's CA layer executor (cad_layer_ctx).
 
@@ -199,7 +215,24 @@ class DistCALayer:
         return int(self.info().launches)
 
     def bind_outputs(self, o: torch.Tensor, lse: torch.Tensor, dq: torch.Tensor) -> None:
+        """No-op kept for the earlier contract (outputs now live in home())."""
         check(lib().cad_layer_ctx_bind_outputs(self._h, o.data_ptr(), lse.data_ptr(), dq.data_ptr()))
+
+    def home(self, layer: int = 0) -> dict:
+        """The layer's home buffers inside the context (zero-copy own rows), as
+        tensors viewing that memory: q, k, v, do, o, dq [home_rows][heads][d]
+        bf16 and lse [h_q][home_rows] fp32. Writing inputs there (and passing
+        None in io) and reading outputs there skips the staging copies."""
+        io = N.cad_layer_io()
+        check(lib().cad_layer_ctx_home(self._h, layer, C.byref(io)))
+        H, d = self.home_rows, self.d
+        out = {}
+        for name, ptr, heads, dt in (("q", io.q, self.hq, torch.bfloat16), ("k", io.k, self.hkv, torch.bfloat16),
+                                     ("v", io.v, self.hkv, torch.bfloat16), ("do", io.dout, self.hq, torch.bfloat16),
+                                     ("o", io.o, self.hq, torch.bfloat16), ("dq", io.dq, self.hq, torch.bfloat16)):
+            out[name] = _wrap(ptr, (H, heads, d), dt, self.dev)
+        out["lse"] = _wrap(io.lse, (self.hq, H), torch.float32, self.dev)
+        return out
 
     def export(self) -> bytes:
         buf = C.create_string_buffer(self.blob_bytes)
