@@ -12,14 +12,14 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind", ["pretrain", "uniform"])
-def test_config3_scale_layer_over_8_ranks_on_one_gpu(kind):
+@pytest.mark.parametrize("kind,world", [("pretrain", 8), ("uniform", 8), ("pretrain", 2), ("pretrain", 4)])
+def test_config3_scale_layer_over_8_ranks_on_one_gpu(kind, world):
     from paper_2510_18121_b200 import configs as CF
     from paper_2510_18121_b200 import dispatch as D
     from paper_2510_18121_b200 import scheduler as S
     from paper_2510_18121_b200.ca import CAPlan, CATaskRows
     dev = torch.device("cuda", 0)
-    world, per = 8, 65536
+    per = 65536
     shape = CF.LLAMA8B
     hq, hkv = shape.h_q, shape.h_kv
     lengths = S.sample_batch(CF.length_dist(kind, 1), world * per)
