@@ -39,6 +39,11 @@ def _timed(fn, steps, stream):
     return t.item(), ms
 
 
+def _log(msg):
+    if os.environ.get("CAD_BENCH_VERBOSE"):
+        print(f"[rank {os.environ.get('RANK', '0')}] {msg}", file=__import__("sys").stderr, flush=True)
+
+
 def run(args, metric, load_peaks, ClockSampler):
     os.environ.setdefault("NCCL_MAX_NCHANNELS", os.environ.get("CAD_NCCL_CHANNELS", "8"))
     rank = int(os.environ.get("RANK", "0"))
@@ -102,6 +107,7 @@ def run(args, metric, load_peaks, ClockSampler):
     def step(L=layer, mode="pingpong", io_=None):
         L.step(io_ or io, mode, comp)
 
+    _log("warmup")
     for _ in range(args.warmup):
         step()
     l0 = layer.launches
@@ -111,12 +117,18 @@ def run(args, metric, load_peaks, ClockSampler):
     clk = clocks.stop()
     launches = layer.launches - l0
     n_side = max(2, args.steps // 2)
+    _log("compute-only")
     ms_compute, my_compute = _timed(lambda: step(mode="compute"), n_side, comp)
+    _log("comm-only")
     ms_comm, _ = _timed(lambda: step(mode="comm"), n_side, comp)
+    _log("signal")
     ms_signal, _ = _timed(lambda: step(mode="signal"), n_side, comp)
+    _log("comm-local")
     ms_comm_local, _ = _timed(lambda: step(mode="comm_local"), n_side, comp)
+    _log("serial")
     ms_serial, _ = _timed(lambda: step(mode="serial"), n_side, comp)
 
+    _log("trace")
     # CAD_TRACE=1: the phase timeline of one ping-pong step on every rank
     traces = None
     if os.environ.get("CAD_TRACE"):
@@ -129,6 +141,7 @@ def run(args, metric, load_peaks, ClockSampler):
         traces = [None] * world
         dist.all_gather_object(traces, tr)
 
+    _log("nccl")
     # NCCL transport (north_star's all-to-allv on a side stream), same
     # schedule and layers, CA grid leaving CAD_NCCL_RESERVE SMs to NCCL
     nccl = None
@@ -153,6 +166,7 @@ def run(args, metric, load_peaks, ClockSampler):
                 "reserve_sms": reserve,
                 "hidden_fraction": max(0.0, min(1.0, 1.0 - (n_ms - n_comp) / n_comm)) if n_comm > 0 else None}
 
+    _log("e2e")
     # e2e: home inputs from pinned host memory, O/LSE/dQ/dK/dV back to host,
     # double-buffered: step j's inputs go host -> device on a copy stream
     # while step j-1 runs, step j's outputs come back while step j+1 runs.
@@ -207,6 +221,7 @@ def run(args, metric, load_peaks, ClockSampler):
     e2e_run(2)
     ms_e2e = e2e_run(max(3, args.steps))
 
+    _log("probe")
     # NVLink probe: one half's forward dispatch (Q + K/V rows this rank pushes
     # into its peers' buffers) alone on a stream, own rows on another stream;
     # achieved GB/s = remote bytes / time of the pushes, per rank

@@ -22,6 +22,7 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_rows.cuh"
+#define CAD_KERNEL_TAG "ca_dq2"
 #include "sm100.cuh"
 
 namespace cad_dev {

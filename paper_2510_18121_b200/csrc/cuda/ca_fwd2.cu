@@ -23,6 +23,7 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_softmax.cuh"
+#define CAD_KERNEL_TAG "ca_fwd2"
 #include "sm100.cuh"
 
 namespace cad_dev {

@@ -22,6 +22,7 @@
 
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
+#define CAD_KERNEL_TAG "comm"
 #include "sm100.cuh"
 
 namespace {

@@ -19,6 +19,9 @@ __device__ __forceinline__ void dbg_mark(int slot, uint32_t code) { g_dbg[blockI
 __device__ __forceinline__ void dbg_mark(int, uint32_t) {}
 #define CAD_DBG_ARGS , 0u, 0u, 0u, 0u
 #endif
+#ifndef CAD_KERNEL_TAG  // names the translation unit in the mbarrier-timeout report
+#define CAD_KERNEL_TAG "?"
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -81,8 +84,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (mbar_try(addr, parity)) return;
     if ((tries & 0xFFFu) == 0 && global_ns() - t0 > 20000000000ull) {
       if ((threadIdx.x & 31) == 0 || threadIdx.x >= 256)
-        printf("cad: mbarrier wait timeout block %d thread %d smem 0x%x parity %u dbg %x %x %x %x\n",
-               blockIdx.x, threadIdx.x, addr, parity CAD_DBG_ARGS);
+        printf("cad: mbarrier wait timeout kernel %s block %d thread %d smem 0x%x parity %u dbg %x %x %x %x\n",
+               CAD_KERNEL_TAG, blockIdx.x, threadIdx.x, addr, parity CAD_DBG_ARGS);
       __trap();
     }
   }
