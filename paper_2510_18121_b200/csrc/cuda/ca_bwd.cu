@@ -21,6 +21,7 @@
 // Both main kernels: 12 warps = elementwise warpgroups 0 and 1 (thread =
 // TMEM lane = tile row), control warpgroup 2 (warp 8 TMA producer, warp 9
 // MMA issuer).
+#define CAD_KERNEL_TAG "ca_bwd"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,7 +34,6 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_rows.cuh"
-#define CAD_KERNEL_TAG "ca_bwd"
 #include "sm100.cuh"
 
 namespace cad_dev {

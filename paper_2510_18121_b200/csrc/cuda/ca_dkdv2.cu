@@ -11,6 +11,7 @@
 // their single-CTA versions). Element-wise work, TMEM layout and MMA order
 // are ca_bwd_dkdv_kernel's (ca_bwd.cu); arrivals go to the even CTA's
 // barriers, and each CTA copies the -LSE/-D rows for its own warpgroups.
+#define CAD_KERNEL_TAG "ca_dkdv2"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -23,7 +24,6 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_rows.cuh"
-#define CAD_KERNEL_TAG "ca_dkdv2"
 #include "sm100.cuh"
 
 namespace cad_dev {

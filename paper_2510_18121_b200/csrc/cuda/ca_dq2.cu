@@ -10,6 +10,7 @@
 // capped and the CTA-pair forward ran 9 % faster than the single-CTA one.
 // Element-wise work is identical to ca_bwd_dq_kernel (ca_bwd.cu); its
 // arrivals go to the even CTA's barriers.
+#define CAD_KERNEL_TAG "ca_dq2"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -22,7 +23,6 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_rows.cuh"
-#define CAD_KERNEL_TAG "ca_dq2"
 #include "sm100.cuh"
 
 namespace cad_dev {
@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         const int hk = un.head0 / p.group;
         const int head = un.head0 + int(rank);
         const int qrow = tk.q_off + un.tile * kTile;
+        dbg_mark(0, 0x1000 + (ui & 0xfff));
         mbar_wait(&bars->q_empty, (q_it & 1) ^ 1);
         ++q_it;
         if (leader) mbar_expect_tx(&bars->q_full, 4 * kTileBytes);
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         tma_load_3d_2sm(&p.tm_do, &bars->q_full, smem + kDOOff + kTileBytes / 2, 64, qrow, head);
         for (int j = 0; j < un.n_kv; ++j) {
           const int krow = tk.kv_off + j * kTile;
+          dbg_mark(0, 0x20000 + (j & 0xffff));
           mbar_wait(&bars->k_empty[kr.i], kr.ph ^ 1);
           if (leader) mbar_expect_tx(&bars->k_full[kr.i], 2 * kKStageBytes);
           else mbar_arrive_leader(&bars->k_full[kr.i]);
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
           tma_load_3d_2sm(&p.tm_k64, &bars->k_full[kr.i], kd + kHalfBytes / 2, 64, krow + 64 * rank, hk);
           tma_load_3d_2sm(&p.tm_k, &bars->k_full[kr.i], kd + kHalfBytes, 64 * rank, krow, hk);
           kr.next();
+          dbg_mark(0, 0x30000 + (j & 0xffff));
           mbar_wait(&bars->v_empty[vr.i], vr.ph ^ 1);
           if (leader) mbar_expect_tx(&bars->v_full[vr.i], 2 * kHalfBytes);
           else mbar_arrive_leader(&bars->v_full[vr.i]);
@@ -207,9 +210,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         const int u = sched_unit(p.sched, n_pairs, ui);
         const FwdUnit un = p.units[u];
         const int n = un.n_kv;
+        dbg_mark(1, 0x10000 + (ui & 0xffff));
         mbar_wait(&bars->q_full, q_it & 1);
         ++q_it;
         const uint32_t sQ = sbase + kQOff, sDO = sbase + kDOOff;
+        dbg_mark(1, 0x20000 + (ui & 0xffff));
         mbar_wait(&bars->k_full[kr.i], kr.ph);
         tc_fence_after();
         issue_ab_pair(tS, sQ, sKk(kr.i));  // S(0)
@@ -224,17 +229,21 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         for (int j = 0; j < n; ++j) {
           const uint32_t kcur = kr.i;
           kr.next();
+          dbg_mark(1, 0x40000 + (j & 0xffff));
           mbar_wait(&bars->p_read, pr_ph);
           pr_ph ^= 1;
           if (j + 1 < n) {
+            dbg_mark(1, 0x50000 + (j & 0xffff));
             mbar_wait(&bars->k_full[kr.i], kr.ph);
             tc_fence_after();
             issue_ab_pair(tS, sQ, sKk(kr.i));  // S(j+1)
             commit_pair(&bars->s_full);
           }
+          dbg_mark(1, 0x60000 + (j & 0xffff));
           mbar_wait(&bars->dp_read, dr_ph);
           dr_ph ^= 1;
           if (j + 1 < n) {
+            dbg_mark(1, 0x70000 + (j & 0xffff));
             mbar_wait(&bars->v_full[vr.i], vr.ph);
             tc_fence_after();
             issue_ab_pair(tDP, sDO, sVk(vr.i));  // dP(j+1)
@@ -245,9 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
             // this unit's last exponentials, dQ MMA and epilogue
             if (j + 2 == n) commit_pair(&bars->q_empty);
           }
+          dbg_mark(1, 0x80000 + (j & 0xffff));
           mbar_wait(&bars->ds_full, ds_ph);
           ds_ph ^= 1;
           if (j == 0) {
+            dbg_mark(1, 0x90000 + (ui & 0xffff));
             mbar_wait(&bars->dq_free, (dq_it & 1) ^ 1);
             ++dq_it;
           }
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
       const int pos = valid ? shift + qi : -1;  // invalid rows see nothing
       const bool all_rows = un.tile * kTile + kTile <= tk.n_q;
       for (int j = 0; j < un.n_kv; ++j) {
+        if (r == 0) dbg_mark(2 + w, 0x10000 + (j & 0xffff));
         mbar_wait_warp(&bars->s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
@@ -309,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
 #pragma unroll
           for (int k = 0; k < 64; ++k) x[k] = k <= lim ? x[k] : 0.f;
         }
+        if (r == 0) dbg_mark(2 + w, 0x20000 + (j & 0xffff));
         mbar_wait_warp(&bars->dp_full, dp_ph);
         dp_ph ^= 1;
         tc_fence_after();
@@ -325,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         tc_fence_before();
         mbar_arrive_leader(&bars->ds_full);
       }
+      if (r == 0) dbg_mark(2 + w, 0x30000 + (ui & 0xffff));
       mbar_wait_warp(&bars->dq_full, dq_ph);
       dq_ph ^= 1;
       tc_fence_after();

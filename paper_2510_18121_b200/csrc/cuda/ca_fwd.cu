@@ -21,6 +21,7 @@
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 // The MMA order PV_h(j) -> S_h(j+1) lets softmax h overlap with the other
 // head's MMAs (ping-pong across the two heads).
+#define CAD_KERNEL_TAG "ca_fwd"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -36,7 +37,6 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_softmax.cuh"
-#define CAD_KERNEL_TAG "ca_fwd"
 #include "sm100.cuh"
 
 namespace cad_dev {

@@ -12,6 +12,7 @@
 // A pair serves 4 query heads of one KV head (GQA group >= 4): CTA r holds
 // heads head0 + 2r + {0,1} in its two softmax warpgroups, exactly like the
 // single-CTA kernel; TMEM per CTA: S0 S1 O0 O1 (512 columns).
+#define CAD_KERNEL_TAG "ca_fwd2"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -23,7 +24,6 @@
 #include "ca_common.cuh"
 #include "ca_mma.cuh"
 #include "ca_softmax.cuh"
-#define CAD_KERNEL_TAG "ca_fwd2"
 #include "sm100.cuh"
 
 namespace cad_dev {

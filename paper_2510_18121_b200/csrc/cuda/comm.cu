@@ -6,6 +6,7 @@
 // NCCL is bound at run time (dlopen of libnccl.so.2): inside a process that
 // already runs torch.distributed this resolves to the NCCL torch loaded, so
 // both communicators share one library.
+#define CAD_KERNEL_TAG "comm"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -22,7 +23,6 @@
 
 #include "../host/cad_status.hpp"
 #include "ca_common.cuh"
-#define CAD_KERNEL_TAG "comm"
 #include "sm100.cuh"
 
 namespace {
