@@ -57,7 +57,12 @@ static_assert(kSmemBytes <= 232448, "dQ pair shared memory");
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full, dp_full, p_read, dp_read, ds_full, dq_full, dq_free;
+  // ds_full per dS buffer (j & 1): the element-wise warps can finish dS(j+1)
+  // before the MMA warp has observed dS(j) -- S(j+1) and dP(j+1) are issued
+  // ahead of that wait -- and one barrier would then complete twice under a
+  // lagging waiter, which then sleeps through both phases (a hang seen under
+  // multi-GPU memory traffic)
+  uint64_t s_full, dp_full, p_read, dp_read, ds_full[2], dq_full, dq_free;
   uint32_t tmem_base;
 };
 
@@ -142,7 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->p_read, 512);
     mbar_init(&bars->dp_read, 512);
-    mbar_init(&bars->ds_full, 512);
+    mbar_init(&bars->ds_full[0], 512);
+    mbar_init(&bars->ds_full[1], 512);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 512);
     fence_barrier_init();
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
       }
     } else if (warp == 9 && leader) {
       // ---------------------------------------------------------- MMA (even CTA)
-      uint32_t q_it = 0, dq_it = 0, pr_ph = 0, dr_ph = 0, ds_ph = 0;
+      uint32_t q_it = 0, dq_it = 0, pr_ph = 0, dr_ph = 0, ds_ph[2] = {0, 0};
       Ring<kKStages> kr;
       Ring<kVStages> vr;
       auto sKk = [&](uint32_t i) { return sbase + kKOff + i * kKStageBytes; };
@@ -255,8 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
             if (j + 2 == n) commit_pair(&bars->q_empty);
           }
           dbg_mark(1, 0x80000 + (j & 0xffff));
-          mbar_wait(&bars->ds_full, ds_ph);
-          ds_ph ^= 1;
+          mbar_wait(&bars->ds_full[j & 1], ds_ph[j & 1]);
+          ds_ph[j & 1] ^= 1;
           if (j == 0) {
             dbg_mark(1, 0x90000 + (ui & 0xffff));
             mbar_wait(&bars->dq_free, (dq_it & 1) ^ 1);
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_pair_kernel(const __gri
         store_bf16_64(tDS + lsel + (j & 1) * 64 + 32 * w, y);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive_leader(&bars->ds_full);
+        mbar_arrive_leader(&bars->ds_full[j & 1]);
       }
       if (r == 0) dbg_mark(2 + w, 0x30000 + (ui & 0xffff));
       mbar_wait_warp(&bars->dq_full, dq_ph);
