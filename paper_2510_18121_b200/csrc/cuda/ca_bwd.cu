@@ -543,7 +543,8 @@ static_assert(kSmemBytes <= 232448, "dQ shared memory");
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full, dp_full, p_read, dp_read, ds_full, dq_full, dq_free;
+  // ds_full per dS buffer (j & 1), see ca_dq2.cu
+  uint64_t s_full, dp_full, p_read, dp_read, ds_full[2], dq_full, dq_free;
   uint32_t tmem_base;
 };
 
@@ -598,7 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->p_read, 256);
     mbar_init(&bars->dp_read, 256);
-    mbar_init(&bars->ds_full, 256);
+    mbar_init(&bars->ds_full[0], 256);
+    mbar_init(&bars->ds_full[1], 256);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 256);
     fence_barrier_init();
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
       // Per iteration j: S(j+1) as soon as the S(j) rows are in registers,
       // dP(j+1) as soon as the dP(j) rows are, then dQ(j) once dS(j) is in
       // TMEM (dS is double-buffered, so dS(j+1) can be written meanwhile).
-      uint32_t q_it = 0, dq_it = 0, pr_ph = 0, dr_ph = 0, ds_ph = 0;
+      uint32_t q_it = 0, dq_it = 0, pr_ph = 0, dr_ph = 0, ds_ph[2] = {0, 0};
       Ring<kKStages> kr;
       Ring<kVStages> vr;
       for (int ui = sched_begin(p.sched, blockIdx.x); ui < sched_end(p.sched, blockIdx.x); ++ui) {
@@ -691,8 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
             mma_commit(&bars->v_empty[vr.i]);
             vr.next();
           }
-          mbar_wait(&bars->ds_full, ds_ph);
-          ds_ph ^= 1;
+          mbar_wait(&bars->ds_full[j & 1], ds_ph[j & 1]);
+          ds_ph[j & 1] ^= 1;
           if (j == 0) {
             mbar_wait(&bars->dq_free, (dq_it & 1) ^ 1);
             ++dq_it;
@@ -769,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dq_kernel(const __grid_con
         store_bf16_64(tDS + lsel + (j & 1) * 64 + 32 * w, y);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars->ds_full);
+        mbar_arrive(&bars->ds_full[j & 1]);
       }
       mbar_wait_warp(&bars->dq_full, dq_ph);
       dq_ph ^= 1;
