@@ -829,6 +829,23 @@ extern "C" int cad_ca_bwd_parts(const cad_ca_plan* plan, const void* q, const vo
       cuda_check(cudaGetLastError(), "ca_delta launch");
       if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_delta");
     }
+    // 2-3 fused (experimental, CAD_BWD_FUSED=1, when the workspace holds the
+    // fp32 dQ accumulator and the plan has pair units): the pair kernel
+    // computes dK, dV and adds the dQ partials into the accumulator
+    // (CAD_BWD_DKDV), the conversion writes dQ (CAD_BWD_DQ).
+    static const bool pair_off = std::getenv("CAD_DKDV_PAIR") && std::getenv("CAD_DKDV_PAIR")[0] == '0';
+    if (fused_bwd_enabled() && !pair_off && ws_bytes >= need + dq_acc_bytes(sh) && !plan->kv2_units.empty()) {
+      float* acc = reinterpret_cast<float*>(static_cast<char*>(workspace) + need);
+      if (parts & CAD_BWD_DKDV) {
+        launch_dkdvq_pair(plan, q, k, v, dout, lse2, delta, pitch, dk, dv, acc, s);
+        if (debug_sync) cuda_check(cudaStreamSynchronize(s), "ca_bwd_dkdvq_pair");
+      }
+      if (parts & CAD_BWD_DQ) {
+        launch_dq_convert(plan, acc, dq, s);
+        if (debug_sync) cuda_check(cudaStreamSynchronize(s), "dq_convert");
+      }
+      return;
+    }
     // 2-3. dK/dV then dQ on `stream`; CAD_BWD_FORK=1 forks dQ onto the plan's
     // side stream (joined back below) so its CTAs take the SMs dK/dV's tail
     // frees -- measured 0.5-1 % slower, hence off by default

@@ -107,6 +107,14 @@ namespace cad_dev {
 // 64 d-values x 128 rows x 1 head, 128-byte swizzle. A 128x128 tile is two
 // boxes (d 0-63 and 64-127), landing as two 16 KB K-major SW128 planes.
 void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, int box_rows = kTile);
+// 3-D map over a packed [rows][heads][128] fp32 buffer (the fused backward's
+// dQ accumulator): box of 32 d-values x 32 rows x 1 head, 128-byte swizzle.
+void make_acc_map(CUtensorMap* map, void* base, int64_t rows, int heads);
+// Bytes of that accumulator (256-byte aligned).
+size_t dq_acc_bytes(const cad_ca_shape& sh);
+// CAD_BWD_FUSED=1: the experimental fused dK/dV/dQ backward (ca_dkdvq2.cu)
+// instead of the two-pass one (slower today).
+bool fused_bwd_enabled();
 // 2-D map over a [heads][rows] fp32 buffer (LSE, D): box of 128 rows x 1 head.
 void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads);
 void cuda_check(cudaError_t e, const char* what);
@@ -124,6 +132,7 @@ void preload_fwd();
 void preload_fwd2();
 void preload_bwd();
 void preload_dkdv2();
+void preload_dkdvq2();
 void preload_dq2();
 void preload_comm();
 // Makes the plan's device current for the duration of a launch (and restores
@@ -140,6 +149,10 @@ bool launch_fwd_pair(const cad_ca_plan* plan, const void* q, const void* k, cons
 bool launch_dkdv_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
                       const float* nlse2, const float* ndelta, int64_t pitch, void* dk, void* dv,
                       cudaStream_t stream);
+bool launch_dkdvq_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
+                       const float* nlse2, const float* ndelta, int64_t pitch, void* dk, void* dv, float* acc,
+                       cudaStream_t stream);
+void launch_dq_convert(const cad_ca_plan* plan, const float* acc, void* dq, cudaStream_t stream);
 bool launch_dq_pair(const cad_ca_plan* plan, const void* q, const void* k, const void* v, const void* dout,
                     const float* lse2, const float* delta, int64_t pitch, void* dq, cudaStream_t stream);
 

@@ -64,6 +64,7 @@ void preload_kernels() {
   preload_fwd2();
   preload_bwd();
   preload_dkdv2();
+  preload_dkdvq2();
   preload_dq2();
   preload_comm();
   // the runtime's own memset / device-to-device copy kernels (the executor's
@@ -118,6 +119,19 @@ void make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int heads, 
                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw cad::CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+void make_acc_map(CUtensorMap* map, void* base, int64_t rows, int heads) {
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(heads)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(heads) * kHeadDim * 4,
+                                 static_cast<cuuint64_t>(kHeadDim) * 4};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cad::CudaError("cuTensorMapEncodeTiled(acc) failed: " + std::to_string(int(r)));
 }
 
 void make_row_map(CUtensorMap* map, const void* base, int64_t rows, int heads) {
@@ -370,7 +384,10 @@ int cad_ca_plan_info_get(const cad_ca_plan* plan, cad_ca_plan_info* info) {
     info->bwd_flops = 10.0 * base;
     // D = rowsum(dO * O) and log2-domain LSE per (head, row), fp32, rows
     // padded to a multiple of 4 (16-byte TMA pitch)
-    info->workspace_bytes = size_t(2) * ((plan->shape.q_rows + 3) / 4 * 4) * plan->shape.h_q * 4;
+    // (+ the experimental fused backward's fp32 dQ accumulator, [rows][h_q]
+    // [128], when CAD_BWD_FUSED=1 selects it; see ca_dkdvq2.cu)
+    info->workspace_bytes = size_t(2) * ((plan->shape.q_rows + 3) / 4 * 4) * plan->shape.h_q * 4 +
+                            (cad_dev::fused_bwd_enabled() ? cad_dev::dq_acc_bytes(plan->shape) : 0);
   });
 }
 
