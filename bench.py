@@ -308,43 +308,54 @@ def single_gpu(args):
     h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, hdo))
     d2h = sum(t.numel() * t.element_size() for t in host_out)
 
-    # Double-buffered: step j's inputs go host -> device on a copy stream while
-    # step j-1 computes, and step j's outputs come back while step j+1
-    # computes; every step still moves its own inputs and results.
+    # Double-buffered over two buffer sets, two copy streams (one per
+    # direction): step j's Q/K/V go host -> device while step j-1 computes,
+    # its dO follows (the backward needs it, the forward does not), its O/LSE
+    # come back while its backward runs and its dQ/dK/dV while step j+1
+    # computes. Every step still moves all of its own inputs and results.
     sets = [(q, k, v, do, o, lse, dq, dk, dv),
             tuple(torch.empty_like(t) for t in (q, k, v, do, o, lse, dq, dk, dv))]
-    copy = torch.cuda.Stream(device=dev)
+    copy_in, copy_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
     def e2e_run(n):
         ev = torch.cuda.Event
-        h2d_done, comp_done = [None, None], [None, None]
+        qkv_in, do_in, fwd_done, bwd_done, out_done = ([None, None] for _ in range(5))
         st, en = ev(enable_timing=True), ev(enable_timing=True)
         torch.cuda.synchronize()
-        st.record(copy)
-        for j in range(n + 1):
-            if j < n:  # inputs of step j
-                b = sets[j % 2]
-                if comp_done[j % 2] is not None:
-                    copy.wait_event(comp_done[j % 2])  # step j-2 done with this set
-                with torch.cuda.stream(copy):
-                    for dst, src in zip(b[:4], (hq, hk, hv, hdo)):
-                        dst.copy_(src, non_blocking=True)
-                h2d_done[j % 2] = ev()
-                h2d_done[j % 2].record(copy)
-            if j >= 1:  # results of step j-1
-                with torch.cuda.stream(copy):
-                    copy.wait_event(comp_done[(j - 1) % 2])
-                    b = sets[(j - 1) % 2]
-                    for dst, src in zip(host_out, b[4:]):
-                        dst.copy_(src, non_blocking=True)
-            if j < n:  # compute step j
-                b = sets[j % 2]
-                stream.wait_event(h2d_done[j % 2])
-                plan.forward(b[0], b[1], b[2], b[4], b[5])
-                plan.backward(b[0], b[1], b[2], b[4], b[5], b[3], b[6], b[7], b[8], ws)
-                comp_done[j % 2] = ev()
-                comp_done[j % 2].record(stream)
-        en.record(copy)
+        st.record(copy_in)
+        for j in range(n):
+            s_, b = j % 2, sets[j % 2]
+            with torch.cuda.stream(copy_in):
+                if bwd_done[s_] is not None:
+                    copy_in.wait_event(bwd_done[s_])  # step j-2 no longer reads this set's inputs
+                for dst, src in zip(b[:3], (hq, hk, hv)):
+                    dst.copy_(src, non_blocking=True)
+                qkv_in[s_] = ev()
+                qkv_in[s_].record(copy_in)
+                b[3].copy_(hdo, non_blocking=True)
+                do_in[s_] = ev()
+                do_in[s_].record(copy_in)
+            stream.wait_event(qkv_in[s_])
+            if out_done[s_] is not None:
+                stream.wait_event(out_done[s_])  # step j-2's results have left this set
+            plan.forward(b[0], b[1], b[2], b[4], b[5])
+            fwd_done[s_] = ev()
+            fwd_done[s_].record(stream)
+            with torch.cuda.stream(copy_out):
+                copy_out.wait_event(fwd_done[s_])
+                for dst, src in zip(host_out[:2], b[4:6]):
+                    dst.copy_(src, non_blocking=True)
+            stream.wait_event(do_in[s_])
+            plan.backward(b[0], b[1], b[2], b[4], b[5], b[3], b[6], b[7], b[8], ws)
+            bwd_done[s_] = ev()
+            bwd_done[s_].record(stream)
+            with torch.cuda.stream(copy_out):
+                copy_out.wait_event(bwd_done[s_])
+                for dst, src in zip(host_out[2:], b[6:]):
+                    dst.copy_(src, non_blocking=True)
+                out_done[s_] = ev()
+                out_done[s_].record(copy_out)
+        en.record(copy_out)
         torch.cuda.synchronize()
         return st.elapsed_time(en) / n
 
