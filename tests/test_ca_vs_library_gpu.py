@@ -1,0 +1,85 @@
+"""Independent numerics cross-check: the CA kernels against a library
+attention implementation in the image (vllm_flash_attn.cute, the sm100
+flash-attention), on the same bf16 inputs.
+
+The reference (the DistCA simulator) has no attention numerics to pin the
+oracle to; the oracle is pinned by fp64 goldens and finite
+differences, and this test adds a second, independently written GPU
+implementation: causal attention with the bottom-right mask, whole documents
+and query shards that attend to their full key prefix (seqlen_k > seqlen_q).
+Test-only: the library is never on the product path. Skipped when the
+library cannot be imported or launched on the box.
+
+Tolerances are the oracle tests' (tests/ca_cases.py), since both sides are
+bf16 outputs of fp32-accumulated kernels."""
+import numpy as np
+import pytest
+import torch
+
+from ca_cases import assert_within, error_report, f32, make_inputs, split_doc, whole_docs
+
+pytestmark = pytest.mark.gpu
+
+
+def _library():
+    try:
+        from vllm.vllm_flash_attn.cute.interface import flash_attn_varlen_func
+        return flash_attn_varlen_func
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"library attention unavailable: {e}")
+
+
+CASES = {
+    # config-2 shape (32 Q / 8 KV heads), whole documents incl. unaligned ones
+    "docs_gqa4": (lambda: whole_docs([300, 1000, 2500, 128]), 32, 8),
+    # one document split into query shards, each attending to its key prefix
+    "shards_gqa4": (lambda: split_doc(3000, [700, 1900]), 32, 8),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_matches_library_attention(name):
+    fa = _library()
+    from paper_2510_18121_b200.ca import CAPlan, CATaskRows
+
+    tasks, rows = CASES[name][0]()
+    h_q, h_kv = CASES[name][1], CASES[name][2]
+    q, k, v = make_inputs(rows, rows, h_q, h_kv, seed=7)
+    g = torch.Generator().manual_seed(8)
+    do = torch.randn(rows, h_q, 128, generator=g).to(torch.bfloat16).cuda()
+
+    plan = CAPlan([CATaskRows(*t) for t in tasks], h_q, h_kv, rows, rows)
+    o, lse = plan.forward(q, k, v)
+    dq, dk, dv = plan.backward(q, k, v, o, lse, do)
+    torch.cuda.synchronize()
+
+    # the library takes one (q, k) sequence pair per task: gather each task's
+    # query rows and its key/value rows (shared prefixes duplicated)
+    qi = torch.cat([torch.arange(t[0], t[0] + t[1]) for t in tasks]).cuda()
+    ki = torch.cat([torch.arange(t[2], t[2] + t[3]) for t in tasks]).cuda()
+    cu_q = torch.tensor([0] + list(np.cumsum([t[1] for t in tasks])), dtype=torch.int32, device="cuda")
+    cu_k = torch.tensor([0] + list(np.cumsum([t[3] for t in tasks])), dtype=torch.int32, device="cuda")
+    ql = q[qi].clone().requires_grad_()
+    kl = k[ki].clone().requires_grad_()
+    vl = v[ki].clone().requires_grad_()
+    try:
+        out = fa(ql, kl, vl, cu_seqlens_q=cu_q, cu_seqlens_k=cu_k, max_seqlen_q=max(t[1] for t in tasks),
+                 max_seqlen_k=max(t[3] for t in tasks), causal=True, return_lse=True)
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"library attention failed to launch: {e}")
+    ol, lsel = out[0], out[1]
+    gq, gk, gv = torch.autograd.grad(ol, (ql, kl, vl), do[qi])
+    torch.cuda.synchronize()
+    # scatter the library's per-task K/V gradients back onto the shared rows
+    dk_l = torch.zeros(rows, h_kv, 128, dtype=torch.float32, device="cuda").index_add_(0, ki, gk.float())
+    dv_l = torch.zeros(rows, h_kv, 128, dtype=torch.float32, device="cuda").index_add_(0, ki, gv.float())
+    lse_l = lsel if lsel.shape[0] == h_q else lsel.transpose(0, 1)  # -> [h_q, total_q]
+
+    qi_np = qi.cpu().numpy()
+    kv_cov = np.unique(ki.cpu().numpy())
+    print(f"{name}: CA kernels vs library attention")
+    assert_within(error_report("o", f32(o)[qi_np], f32(ol)))
+    assert_within(error_report("lse", f32(lse)[:, qi_np].T, f32(lse_l).T))
+    assert_within(error_report("dq", f32(dq)[qi_np], f32(gq)))
+    assert_within(error_report("dk", f32(dk)[kv_cov], f32(dk_l)[kv_cov]))
+    assert_within(error_report("dv", f32(dv)[kv_cov], f32(dv_l)[kv_cov]))
