@@ -64,6 +64,7 @@ constexpr uint32_t kEmuMask = CAD_KVQ2_EMU_MASK;
 #endif
 constexpr bool kNoReduce = CAD_KVQ2_DIAG & 1, kNoDstWait = CAD_KVQ2_DIAG & 2, kNoDqMma = CAD_KVQ2_DIAG & 4;
 constexpr bool kNoDqFree = CAD_KVQ2_DIAG & 8, kNoXchg = CAD_KVQ2_DIAG & 16;
+constexpr bool kNoExchange = CAD_KVQ2_DIAG & 32, kNoReadout = CAD_KVQ2_DIAG & 64;
 #ifndef CAD_KVQ2_DQ_FIRST
 #define CAD_KVQ2_DQ_FIRST 0
 #endif
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdvq_pair_kernel(const __
           commit_pair(&bars->qm_empty);
           // dQ(i) into dP^T's columns [0, 64) once both CTAs hold dS(i)
           if (i == 0) mbar_wait(&bars->kq_full, kv_it & 1);
-          mbar_wait(&bars->xchg_ready, nq & 1);
+          if (!kNoExchange) mbar_wait(&bars->xchg_ready, nq & 1);
           tc_fence_after();
           if (!kNoDqMma) issue_dq_pair(tDP, sDs + (nq & 1) * kTileBytes, sKq);
           commit_pair(&bars->dq_full);
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdvq_pair_kernel(const __
       // The peer's dS half lands here by st.async (complete_tx on xchg_full);
       // once all 16 KB are in, make them visible to the async proxy and tell
       // the MMA issuer (xchg_ready on the even CTA, one arrival per CTA).
-      if (lane == 0) {
+      if (lane == 0 && !kNoExchange) {
         uint32_t it = 0;
         for (int ui = sched_begin(p.sched, pair); ui < sched_end(p.sched, pair); ++ui) {
           const int n = p.units[sched_unit(p.sched, n_pairs, ui)].n_iter;
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdvq_pair_kernel(const __
           mbar_wait_warp(&bars->dq_full, it & 1);
           tc_fence_after();
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
+          for (int b = 0; b < 2 && !kNoReadout; ++b) {
             uint32_t v[32];
             tmem_ld32(tq + 32 * b, v);
             tmem_wait_ld();
@@ -534,6 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdvq_pair_kernel(const __
             for (int c4 = 0; c4 < 8; ++c4)
               *reinterpret_cast<uint4*>(line + ((c4 ^ (lane & 7)) << 4)) =
                   make_uint4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+          }
+          if (kNoReadout) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&bars->dq_free);
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -688,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) ca_bwd_dkdvq_pair_kernel(const __
           // iteration's partial has left both CTAs' staging
           if (ch == 0 && !kNoDstWait) mbar_wait_warp(&bars->dst_free[it & 1], ((it >> 1) & 1) ^ 1);
           const uint32_t dsb = (it & 1) * kTileBytes;
-          if (kNoXchg) {
+          if (kNoXchg || kNoExchange) {
           } else if (uint32_t(ch) == rank) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
