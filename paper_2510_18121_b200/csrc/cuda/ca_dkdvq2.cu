@@ -1,16 +1,19 @@
-// Fused dK/dV/dQ on CTA pairs (cta_group::2): the pair dK/dV kernel of
-// ca_dkdv2.cu plus dQ = dS K accumulated in the same pass, so the backward
-// no longer recomputes S and dP in a separate dQ kernel (5 tile GEMMs per
-// (kv tile pair, q tile, head) instead of 7).
+// Fused dK/dV/dQ on CTA pairs (cta_group::2), EXPERIMENTAL (CAD_BWD_FUSED=1;
+// measured slower than the two-pass backward, profiles/r2_fused_bwd.md): the
+// pair dK/dV kernel of ca_dkdv2.cu plus dQ = dS K accumulated in the same
+// pass, so the backward does not recompute S and dP in a separate dQ kernel
+// (5 tile GEMMs per (kv tile pair, q tile, head) instead of 7).
 //
 //   dQ(i) [q 128 x d 128] = dS(i) [q x 256 kv of the pair] K [256 kv x d]
 // is one M=128 cta_group::2 MMA per iteration whose reduction runs over both
 // CTAs' kv rows, so the pair adds ONE fp32 partial per (q tile, head) into
 // the accumulator instead of two:
 //   A: CTA r holds q rows [64r, 64r+64) of dS for all 256 kv rows (MN-major
-//      SW128, 32 KB). The element-wise threads of BOTH CTAs write it: a
-//      thread's q chunk ch (its kv row, q columns [64ch + 32w, +32)) goes to
-//      CTA ch's buffer, the remote half over DSMEM.
+//      SW128, 32 KB, double-buffered by iteration parity). The element-wise
+//      threads of BOTH CTAs write it: a thread's q chunk ch (its kv row, q
+//      columns [64ch + 32w, +32)) goes to CTA ch's buffer -- locally, or by
+//      st.async with complete_tx on the peer's xchg_full barrier, which a
+//      relay warp turns into an arrival on the MMA issuer's xchg_ready.
 //   B: CTA r holds d columns [64r, 64r+64) of both kv tiles' K rows (a second,
 //      MN-major view of K: one 16 KB plane per tile).
 //   D: CTA r's TMEM lanes [0,64) = q 64r+lane, d [0,64); lanes [64,128) =
@@ -18,23 +21,25 @@
 //      64 columns: the half of dP^T's columns the packed dS^T leaves free
 //      (dS^T is packed into columns [64,128), P^T stays where ca_dkdv2 has it).
 // Four reduce warps read the partial out (which frees the columns for
-// dP^T(i+1)), stage it in the dS buffer (idle once dQ(i) has completed) and
-// add it into an fp32 [rows][h_q][128] accumulator with TMA reduce-adds
-// (cp.reduce.async.bulk.tensor .add.f32; ~6 TB/s of L2 reductions measured,
-// scripts/micro/l2_reduce.cu). Rows past a task's queries receive +0 (their
-// dS is masked) and rows past the buffer are clipped by TMA. The host zeroes
-// the accumulator before the launch and a conversion kernel writes
-// scale * accumulator as bf16 dQ after it. fp32 addition order varies from
-// run to run: the two-pass backward (ca_dkdv2 + ca_dq2) stays the
-// deterministic mode.
+// dP^T(i+1)), stage it in that iteration's dS buffer (idle once dQ(i) has
+// completed) and add it into an fp32 [rows][h_q][128] accumulator with TMA
+// reduce-adds (cp.reduce.async.bulk.tensor .add.f32; ~6 TB/s of L2
+// reductions measured, scripts/micro/l2_reduce.cu). Rows past a task's
+// queries receive +0 (their dS is masked) and rows past the buffer are
+// clipped by TMA. The host zeroes the accumulator before the launch and a
+// conversion kernel writes scale * accumulator as bf16 dQ after it. fp32
+// addition order varies from run to run: the two-pass backward (ca_dkdv2 +
+// ca_dq2) is the default and deterministic.
 //
-// Shared memory per CTA: K, V (32 KB each), 2 Q stages, 1 dO stage (32 KB
-// each: K-major rows [64r, 64r+64) + MN-major columns [64r, 64r+64) as in
-// ca_dkdv2), the dQ view of K (32 KB), dS / reduce staging (32 KB): 226 KB.
-// dK/dV leave by direct global stores (no staging left for TMA stores).
+// Shared memory per CTA: K, V (32 KB each), one Q and one dO tile (32 KB
+// each, as two independently released halves: K-major rows [64r, 64r+64)
+// for S^T / dP^T, MN-major columns [64r, 64r+64) for dK / dV; the producer
+// runs one iteration ahead), the dQ view of K (32 KB), two dS / staging
+// buffers (64 KB): 226 KB. dK/dV leave by direct global stores.
 //
 // Warps: 0-7 element-wise (thread = kv row), 8 TMA producer, 9 MMA issuer
-// (even CTA), 10-11 idle, 12-15 dQ reduce (TMEM quadrant = warp % 4).
+// (even CTA), 10 dS relay, 11 idle, 12-15 dQ reduce (TMEM quadrant =
+// warp % 4).
 #define CAD_KERNEL_TAG "ca_dkdvq2"  // names this file in the mbarrier-timeout report
 #include <cuda.h>
 #include <cudaTypedefs.h>
