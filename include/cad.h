@@ -283,7 +283,7 @@ typedef struct cad_ca_task {
 
 /* Packed THD layouts: Q/O/dO [q_rows][h_q][head_dim] bf16, K/V/dK/dV
  * [kv_rows][h_kv][head_dim] bf16, LSE [h_q][q_rows] fp32 (natural log),
- * dQ accumulated in fp32 workspace then written bf16. head_dim must be 128.
+ * all accumulation fp32 (in TMEM), outputs written bf16. head_dim must be 128.
  * softmax_scale <= 0 selects 1/sqrt(head_dim). */
 typedef struct cad_ca_shape {
   int32_t h_q;
@@ -302,7 +302,9 @@ typedef struct cad_ca_plan_info {
   int64_t causal_pairs;   /* sum over tasks of exact causal pairs */
   double fwd_flops;       /* 4 * d * h_q * pairs */
   double bwd_flops;       /* 10 * d * h_q * pairs */
-  size_t workspace_bytes; /* bytes cad_ca_bwd needs */
+  size_t workspace_bytes; /* bytes cad_ca_bwd needs (+ an fp32 dQ accumulator
+                             when CAD_BWD_FUSED=1 selects the experimental
+                             fused backward) */
 } cad_ca_plan_info;
 
 int cad_ca_plan_create(const cad_ca_task* tasks, int64_t n_tasks,
@@ -330,7 +332,9 @@ int cad_ca_bwd(const cad_ca_plan* plan, const void* q, const void* k,
 
 /* The backward's launches, separately: D = rowsum(dO*O) (+ log2 LSE) into the
  * workspace, then dK/dV and dQ, which only depend on the workspace and may
- * run on different streams once DELTA has completed. */
+ * run on different streams once DELTA has completed. With CAD_BWD_FUSED=1
+ * (experimental, not deterministic) CAD_BWD_DKDV also adds the dQ partials
+ * into the workspace's fp32 accumulator and CAD_BWD_DQ converts it. */
 #define CAD_BWD_DELTA 1
 #define CAD_BWD_DKDV 2
 #define CAD_BWD_DQ 4
