@@ -192,6 +192,11 @@ def reference_arm(args, rank):
     tf = statistics.mean(v[0] for v in vals)
     ms = statistics.mean(v[1] for v in vals) * 1e3
     sample = _cfg1_sample(1) + " per step"
+    # the config our own arm reports for the same launch (bench.py at N=1,
+    # bench_dist.py at N>1), which this CPU sample stands in for
+    workload = os.environ.get("CAD_WORKLOAD", "cfg2" if args.gpus <= 1 else "cfg3")
+    wl_name = (CFG2_WORKLOAD if workload == "cfg2"
+               else f"the {workload} workload of this bench's own arm at {args.gpus} GPU(s)")
     try:
         sched = ref_scheduler_ms_cfg3()
     except Exception as e:  # reference library absent
