@@ -128,7 +128,9 @@ def run_cpu_oracle(lengths, h_q=1, h_kv=1, threads=0, reps=1):
     k = rng.standard_normal((T, h_kv, 128), dtype=np.float32)
     v = rng.standard_normal((T, h_kv, 128), dtype=np.float32)
     do = rng.standard_normal((T, h_q, 128), dtype=np.float32)
-    nthreads = threads or oracle.num_lib().oracle_max_threads()
+    # every host core this process may use (torchrun exports OMP_NUM_THREADS=1
+    # to its workers, which would otherwise cap the OpenMP oracle at one thread)
+    nthreads = threads or max(oracle.num_lib().oracle_max_threads(), len(os.sched_getaffinity(0)))
     t0 = time.perf_counter()
     for _ in range(reps):
         o, _lse = oracle.ca_forward(tasks, q, k, v, threads=nthreads)
