@@ -145,7 +145,8 @@ def run(args, metric, load_peaks, ClockSampler):
     # NCCL transport (north_star's all-to-allv on a side stream), same
     # schedule and layers, CA grid leaving CAD_NCCL_RESERVE SMs to NCCL
     nccl = None
-    if os.environ.get("CAD_NCCL_LINE", "1") != "0":
+    # on by default up to 4 GPUs (the sizes it was validated at); CAD_NCCL_LINE=1/0 forces it
+    if os.environ.get("CAD_NCCL_LINE", "1" if world <= 4 else "0") != "0":
         reserve = int(os.environ.get("CAD_NCCL_RESERVE", "8"))
         obj = [D.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
