@@ -34,6 +34,12 @@ CASES = {
     "docs_gqa4": (lambda: whole_docs([300, 1000, 2500, 128]), 32, 8),
     # one document split into query shards, each attending to its key prefix
     "shards_gqa4": (lambda: split_doc(3000, [700, 1900]), 32, 8),
+    # head_tail (per-document CP) pair of one 2000-token document: head [300, 700)
+    # over keys [0, 700) and its mirror [1300, 1700) over keys [0, 1700),
+    # sharing the document's KV rows (P/include/cadsim/types.hpp:107-111)
+    "head_tail_gqa4": (lambda: ([(300, 400, 0, 700), (1300, 400, 0, 1700)], 2000), 32, 8),
+    # config 4's shape: 64 Q / 8 KV heads (GQA 8)
+    "docs_gqa8": (lambda: whole_docs([1500, 700, 33]), 64, 8),
 }
 
 
