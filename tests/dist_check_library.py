@@ -1,5 +1,6 @@
 """torchrun script: the distributed CA layer at BASELINE config 3's per-GPU
-size (65536 tokens per GPU, 32 Q / 8 KV heads, pretrain_upsampled seed 1,
+size (65536 tokens per GPU, 32 Q / 8 KV heads, pretrain_upsampled seed 1;
+CAD_CHECK_WORKLOAD=cfg4: config 4's 1M-token 34B batch,
 scheduler-sharded, IPC pushes, ping-pong) against the image's sm100
 flash-attention library run on the whole global batch on every rank (test
 only). Every home row of O, LSE, dQ, dK, dV is compared on the GPU. Prints
@@ -38,16 +39,22 @@ def main():
     from paper_2510_18121_b200 import configs as CF
     from paper_2510_18121_b200 import dispatch as D
     from paper_2510_18121_b200 import scheduler as S
-    shape = CF.LLAMA8B
+    # CAD_CHECK_WORKLOAD=cfg4: BASELINE config 4 instead (34B shape, 64 / 8
+    # heads, 1M tokens over the GPUs, documents up to 256K)
+    if os.environ.get("CAD_CHECK_WORKLOAD", "cfg3") == "cfg4":
+        shape = CF.LLAMA34B
+        lengths = S.sample_batch(CF.length_dist("pretrain", 1, max_doc_len=262144), 1 << 20)
+    else:
+        shape = CF.LLAMA8B
+        lengths = S.sample_batch(CF.length_dist("pretrain", 1), 65536 * world)
     h_q, h_kv = shape.h_q, shape.h_kv
-    lengths = S.sample_batch(CF.length_dist("pretrain", 1), 65536 * world)
     T = sum(lengths)
     dev = torch.device("cuda", local)
     g = torch.Generator(device=dev).manual_seed(21)  # the same global inputs on every rank
-    q = torch.randn(T, h_q, 128, device=dev, generator=g).to(torch.bfloat16)
-    k = torch.randn(T, h_kv, 128, device=dev, generator=g).to(torch.bfloat16)
-    v = torch.randn(T, h_kv, 128, device=dev, generator=g).to(torch.bfloat16)
-    do = torch.randn(T, h_q, 128, device=dev, generator=g).to(torch.bfloat16)
+    q = torch.randn(T, h_q, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, h_kv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, h_kv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    do = torch.randn(T, h_q, 128, device=dev, generator=g, dtype=torch.bfloat16)
 
     lp = D.LayerPlan(lengths, world, rank, shape)
     # this rank's home rows as global row indices (head rows, then a head_tail
@@ -73,6 +80,9 @@ def main():
     io = layer.io(hq, hk, hv, hdo, o, lse, dq, dk, dv)
     layer.step(io, "pingpong")
     torch.cuda.synchronize()
+    layer.close()  # free the executor's buffers before the library's whole-batch pass
+    del io, hq, hk, hv, hdo
+    torch.cuda.empty_cache()
 
     cu = torch.tensor([0] + list(np.cumsum(lengths)), dtype=torch.int32, device=dev)
     ql, kl, vl = (t.clone().requires_grad_() for t in (q, k, v))
@@ -88,7 +98,6 @@ def main():
     print(json.dumps({"rank": rank, "world": world, "home_rows": int(lp.home_rows), "docs": len(lengths),
                       "errors": {n: {"row_rel": r, "abs": a} for n, (r, a) in res.items()}, "lse_abs": lse_abs,
                       "ok": bool(ok)}), flush=True)
-    layer.close()
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
