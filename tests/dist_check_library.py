@@ -70,17 +70,27 @@ def main():
     rows = torch.from_numpy(np.concatenate(idx)).to(dev)
     assert rows.numel() == lp.home_rows
 
-    layer = D.DistCALayer(lp, dev, "ipc")
+    transport = os.environ.get("CAD_TRANSPORT", "ipc")  # ipc | nccl
+    layer = D.DistCALayer(lp, dev, transport, reserve_sms=8 if transport == "nccl" else 0)
     hq, hk, hv, hdo = (t[rows].contiguous() for t in (q, k, v, do))
     o = torch.empty_like(hq)
     lse = torch.empty(h_q, lp.home_rows, device=dev)
     dq, dk, dv = torch.empty_like(hq), torch.empty_like(hk), torch.empty_like(hv)
-    layer.bind_outputs(o, lse, dq)
-    layer.connect_dist()
+    comm = None
+    if transport == "nccl":
+        obj = [D.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = D.Comm(obj[0], rank, world)
+        layer.set_comm(comm)
+    else:
+        layer.bind_outputs(o, lse, dq)
+        layer.connect_dist()
     io = layer.io(hq, hk, hv, hdo, o, lse, dq, dk, dv)
     layer.step(io, "pingpong")
     torch.cuda.synchronize()
     layer.close()  # free the executor's buffers before the library's whole-batch pass
+    if comm is not None:
+        comm.close()
     del io, hq, hk, hv, hdo
     torch.cuda.empty_cache()
 
@@ -95,7 +105,8 @@ def main():
            "dv": _row_rel(dv, gv[rows])}
     lse_abs = float((lse - lse_l[:, rows]).abs().max())
     ok = res["o"][1] <= 2e-2 and lse_abs <= 1e-3 and all(res[n][0] <= 2e-2 for n in ("dq", "dk", "dv"))
-    print(json.dumps({"rank": rank, "world": world, "home_rows": int(lp.home_rows), "docs": len(lengths),
+    print(json.dumps({"rank": rank, "world": world, "transport": transport, "home_rows": int(lp.home_rows),
+                      "docs": len(lengths),
                       "errors": {n: {"row_rel": r, "abs": a} for n, (r, a) in res.items()}, "lse_abs": lse_abs,
                       "ok": bool(ok)}), flush=True)
     dist.barrier()

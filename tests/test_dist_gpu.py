@@ -34,17 +34,17 @@ def test_distributed_layer(world, transport, layers):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_layer_config3_vs_library(world):
+@pytest.mark.parametrize("world,transport", [(2, "ipc"), (2, "nccl"), (4, "ipc")])
+def test_distributed_layer_config3_vs_library(world, transport):
     """BASELINE config 3's per-GPU size (65536 tokens per GPU, 32 / 8 heads)
     through the executor, every home row against the library attention on
     the whole batch (tests/dist_check_library.py)."""
     if _n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(world),
-                        "--master-addr", "127.0.0.1", "--master-port", str(29611 + world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(29611 + world + 7 * (transport == "nccl")),
                         os.path.join(HERE, "dist_check_library.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900, env=dict(os.environ, CAD_TRANSPORT=transport))
     print(r.stdout[-6000:])
     if '"skip"' in r.stdout:
         pytest.skip("library attention unavailable")
